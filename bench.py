@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""bench.py -- MOM mini-sequence prefill MLP path on B200 (arXiv 2504.12526).
+
+One STEP is one pass of the whole hot path (a11 when N > 1) over one
+batch of synthetic input, in Alg. 1's order, at BASELINE config 2 shapes
+(Llama-3-8B MLP: hidden 4096, intermediate 14336, vocab 128256, S = 65536 tokens per GPU,
+M = 8 mini-sequences, bf16):
+  a9   KV offload of the layer's K/V [S, 2*1024] bf16 to pinned host (side stream), overlapping
+  a1-4 the mini-sequence SwiGLU MLP of a non-final layer (tcgen05, M launches of phase A + B)
+  a11  (N > 1) in-place NCCL all-gather of the MLP output rows
+  a6   the final layer's MLP on the last token only (GEMV pair)          } on the rank that
+  a7-8 LM head on the last token + final RMSNorm + greedy argmax (GEMV)   } owns token S-1
+  a10  reload of the offloaded KV (H2D) after the head, as Alg. 1 P:106 orders it.
+Inputs are resident in HBM and larger than L2 (x 537 MB, weights 352 MB per layer).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
+For N > 1 launch with torch.distributed.run (one process per GPU).  Rank 0 prints ONE JSON
+line.  `--impl reference` times the CPU oracle (oracle/, the only baseline this paper-only
+tier has) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return dict(PEAKS_FALLBACK), "fallback (B200_PROFILING.md)"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["mine", "reference"], default="mine")
+    ap.add_argument("--config", type=int, default=1, help="index into BASELINE.json configs (default 1 = config 2)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- distributed
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        backend = "nccl" if torch.cuda.is_available() and args.impl == "mine" else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int, device) -> float:
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int, device) -> float:
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and clock-event (throttle) reasons with NVML during the timed region."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting",
+               0x10: "sync_boost"}
+
+    def __init__(self, device_index: int, period_s: float = 0.02):
+        self.period = period_s
+        self.samples, self.reasons, self.max_mhz, self.power = [], set(), None, []
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _reasons(self):
+        nv = self.nv
+        fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        return fn(self.h)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self._reasons()
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self._ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml-unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "power_w_max": max(self.power) if self.power else None}
+
+
+# ----------------------------------------------------------------------------- workload
+class Workload:
+    """Device-resident inputs of one rank (weak scaling: S tokens per GPU)."""
+
+    def __init__(self, cfg, rank, world, device):
+        self.cfg, self.rank, self.world, self.device = cfg, rank, world, device
+        d, I, V, S, C = cfg.hidden, cfg.intermediate, cfg.vocab, cfg.S, cfg.C
+        bf = torch.bfloat16
+        self.S, self.C, self.d, self.I, self.V = S, C, d, I, V
+        self.M = math.ceil(S / C)
+        # layer 0: a non-final (mini-sequence) layer; layer L-1: the final (last-token) layer
+        self.w0 = synth.mlp_weights(d, I, 0, device, bf)
+        self.w1 = synth.mlp_weights(d, I, cfg.layers - 1, device, bf)
+        self.wh = synth.head_weight(V, d, device, bf)
+        self.gain = synth.norm_gain(d, device, bf)
+        self.x = synth.hidden(S, d, device, bf, seed=synth.SEED_X + rank)
+        self.kv = synth.kv_standin(S, cfg.d_kv, rank, device, bf)  # stand-in for attention's K/V
+        self.kv_host = torch.empty(self.kv.shape, dtype=bf, pin_memory=True)
+        self.kv_back = torch.empty_like(self.kv)
+        self.out = torch.empty((world * S, d), dtype=bf, device=device)  # gathered rows when world > 1
+        from paper_2504_12526_b200 import _mom
+        self.ws = torch.empty(_mom.mlp_minseq_workspace_bytes(S, d, I, C, bf), dtype=torch.uint8, device=device)
+        self.ws_last = torch.empty(_mom.lib().mom_mlp_last_token_workspace_bytes(I), dtype=torch.uint8, device=device)
+        self.ws_head = torch.empty(_mom.lib().mom_lm_head_workspace_bytes(V), dtype=torch.uint8, device=device)
+        self.y = torch.empty(d, dtype=bf, device=device)
+        self.logits = torch.empty(V, dtype=torch.float32, device=device)
+        self.argmax = torch.empty(1, dtype=torch.int32, device=device)
+        self.owns_last = rank == world - 1
+        self.comm = None
+
+    @property
+    def shard(self):
+        return self.out[self.rank * self.S:(self.rank + 1) * self.S]
+
+
+def run_step(wl, compute, copy, launches):
+    """One pass of the hot path, enqueued on `compute` (MLP, head) and `copy` (KV copies)."""
+    from paper_2504_12526_b200 import _mom
+    copy.wait_stream(compute)
+    _mom.kv_offload(wl.kv, wl.kv_host, compute, copy)                                   # a9
+    wg, wu, wd = wl.w0
+    _mom.mlp_minseq_fwd(wl.x, wl.x, wg, wu, wd, wl.shard, wl.C, wl.ws, compute)         # a1-a4
+    launches[0] += 2 * wl.M
+    if wl.world > 1:
+        _mom.allgather_rows(wl.out, wl.S, wl.comm, wl.rank, wl.world, compute)           # a11
+    if wl.owns_last:
+        last = wl.out[wl.world * wl.S - 1]
+        wg1, wu1, wd1 = wl.w1
+        _mom.mlp_last_token(last, last, wg1, wu1, wd1, wl.y, wl.ws_last, compute)        # a6
+        _mom.lm_head_last(wl.y, wl.gain, wl.cfg.eps, wl.wh, wl.logits, wl.argmax, wl.ws_head, compute)  # a7-a8
+        launches[0] += 4
+    copy.wait_stream(compute)  # Alg. 1: the reload follows the head
+    _mom.kv_reload(wl.kv_host, wl.kv_back, copy)                                        # a10
+    compute.wait_stream(copy)
+
+
+def measure_peak_activation(wl, C):
+    """Peak extra device bytes of one mini-sequence MLP call (workspace allocated by the call)."""
+    from paper_2504_12526_b200 import _mom
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    wg, wu, wd = wl.w0
+    _mom.mlp_minseq_fwd(wl.x, wl.x, wg, wu, wd, wl.shard, C)
+    torch.cuda.synchronize()
+    return torch.cuda.max_memory_allocated() - base
+
+
+def cpu_baseline(wl, target_s: float = 12.0):
+    """The oracle as it stands on a bounded sample of the workload (rows of the MLP layer)."""
+    import oracle
+    threads = oracle.default_threads()
+    wg, wu, wd = (t.cpu() for t in wl.w0)
+    x = wl.x.cpu()
+    # calibrate with one row per thread, then size the sample for ~target_s of CPU time
+    rows = synth.sample_rows(wl.S, wl.C, n_random=threads)[:threads]
+    t0 = time.perf_counter()
+    oracle.mlp_rows(x, x, wg, wu, wd, rows, nthreads=threads)
+    t1 = time.perf_counter() - t0
+    reps = max(1, min(8, int(target_s / max(t1, 1e-3))))
+    rows2 = synth.sample_rows(wl.S, wl.C, n_random=threads * reps, seed=synth.SEED_ROWS + 1)[:threads * reps]
+    t0 = time.perf_counter()
+    oracle.mlp_rows(x, x, wg, wu, wd, rows2, nthreads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": len(rows2) / dt, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+            "sample": f"{len(rows2)} sampled rows of the layer-0 MLP (config 2 shapes, float64 C oracle, "
+                      f"{dt:.1f} s); the last-token path is amortised over S and excluded"}
+
+
+def run_mine(args):
+    world, rank, local = dist_setup(args)
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product has no CPU path)")
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    from paper_2504_12526_b200 import _mom
+    from paper_2504_12526_b200 import build as _build
+    if not os.path.exists(_mom.LIB_PATH):
+        _build.build()
+    cfg = synth.CONFIGS[args.config]
+    peaks, peaks_src = load_peaks()
+    wl = Workload(cfg, rank, world, device)
+    if world > 1:
+        uid = _mom.nccl_get_unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        wl.comm = _mom.nccl_comm_init(world, obj[0], rank)
+    compute = torch.cuda.Stream(device)
+    copy = torch.cuda.Stream(device)
+    torch.cuda.synchronize()
+
+    # warm-up (untimed)
+    dummy = [0]
+    with torch.cuda.stream(compute):
+        for _ in range(args.warmup):
+            run_step(wl, compute, copy, dummy)
+    torch.cuda.synchronize()
+
+    # timed region: K steps, barrier + sync on both sides, CUDA events on the compute stream
+    launches = [0]
+    timer = _mom.LaunchTimer(capacity=max(64, args.steps * (2 * wl.M + 2) + 8))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(device.index) as clk, timer, torch.cuda.stream(compute):
+        ev0.record(compute)
+        for _ in range(args.steps):
+            run_step(wl, compute, copy, launches)
+        ev1.record(compute)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ms_local, world, device)
+    total_tokens = world * wl.S
+    value = total_tokens / (ms / 1e3)
+    n_launch = int(sum_over_ranks(launches[0], world, device))
+
+    # per-kernel times (live, same timed region)
+    per = {}
+    for kind, t in timer.results():
+        per.setdefault(kind, []).append(t)
+    d, I, C, S = wl.d, wl.I, wl.C, wl.S
+    flops_a = 4.0 * C * d * I      # gate + up projections of one mini-sequence (2 GEMMs, 2 flop/MAC)
+    flops_b = 2.0 * C * d * I      # down projection
+    ta = statistics.mean(per["phaseA_tc"]) if "phaseA_tc" in per else float("nan")
+    tb = statistics.mean(per["phaseB_tc"]) if "phaseB_tc" in per else float("nan")
+    sustained = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
+    burst = peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"])
+    hbm = peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
+    ach_a = flops_a / (ta * 1e-3) / 1e12
+    ach_b = flops_b / (tb * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "phaseA_dram_bytes.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    kernels = {"phaseA_tc": {"ms": ta, "tflops": ach_a, "frac_sustained": ach_a / sustained},
+               "phaseB_tc": {"ms": tb, "tflops": ach_b, "frac_sustained": ach_b / sustained}}
+    if "last_token_gemv" in per:
+        t = statistics.mean(per["last_token_gemv"])
+        gbs = 3.0 * d * I * 2 / (t * 1e-3) / 1e9
+        kernels["last_token_gemv"] = {"ms": t, "gbs": gbs, "frac_hbm": gbs / hbm}
+    if "lm_head_gemv" in per:
+        t = statistics.mean(per["lm_head_gemv"])
+        gbs = 1.0 * wl.V * d * 2 / (t * 1e-3) / 1e9
+        kernels["lm_head_gemv"] = {"ms": t, "gbs": gbs, "frac_hbm": gbs / hbm}
+    mlp_ms = wl.M * (ta + tb)
+
+    result = {
+        "metric": "prefill MLP tokens/s (MOM mini-sequence path: KV offload + M-chunk SwiGLU MLP + last-token MLP/LM head/argmax + KV reload)",
+        "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (seeded random-init weights and inputs, synth/)",
+        "config": {"workload": cfg.name, "hidden": d, "intermediate": I, "vocab": wl.V,
+                   "seq_len_per_gpu": S, "global_tokens": total_tokens, "minseq_len": C, "M": wl.M,
+                   "kv_bytes_per_layer": wl.kv.numel() * 2, "parallelism": f"token-shard x{world}",
+                   "l2": "inputs larger than L2 (x 537 MB, weights 352 MB/layer, W_head 1.05 GB)"},
+        "roofline": {"kernel": "phaseA_tc (gate/up GEMM + SiLU*mul, tcgen05)", "bound": "tensor",
+                     "achieved": ach_a, "peak": sustained, "unit": "TFLOP/s", "frac": ach_a / sustained,
+                     "traffic": traffic, "peak_source": peaks_src + " bf16_tflops_sustained (kernel timed inside a long step)",
+                     "frac_of_burst_peak": ach_a / burst, "flop_per_launch": flops_a},
+        "kernels": kernels,
+        "mlp_only": {"ms": mlp_ms, "tokens_per_s": S / (mlp_ms * 1e-3),
+                     "tflops": 6.0 * S * d * I / (mlp_ms * 1e-3) / 1e12,
+                     "frac_sustained": 6.0 * S * d * I / (mlp_ms * 1e-3) / 1e12 / sustained},
+        "gpu_launches": n_launch,
+    }
+    result["clocks"] = clk.summary()
+
+    # peak activation (Eq. 1 P:158 vs Eq. 3), outside the timed region
+    if rank == 0:
+        pa = measure_peak_activation(wl, C)
+        result["peak_activation_gb"] = pa / 1e9
+        result["peak_activation_unchunked_eq1_gb"] = S * I * 2 / 1e9
+        result["activation_reduction_x"] = (S * I * 2) / max(pa, 1)
+
+    # end to end through the public API with host buffers (H2D of x, D2H of logits + token)
+    if not args.no_e2e:
+        x_host = wl.x.cpu().pin_memory()
+        lg_host = torch.empty(wl.V, dtype=torch.float32, pin_memory=True)
+        am_host = torch.empty(1, dtype=torch.int32, pin_memory=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(compute):
+            e0.record(compute)
+            for _ in range(args.steps):
+                wl.x.copy_(x_host, non_blocking=True)
+                run_step(wl, compute, copy, [0])
+                if wl.owns_last:
+                    lg_host.copy_(wl.logits, non_blocking=True)
+                    am_host.copy_(wl.argmax, non_blocking=True)
+            e1.record(compute)
+            torch.cuda.synchronize()
+        e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, device)
+        result["e2e"] = {"value": total_tokens / (e_ms / 1e3), "unit": "tokens/s",
+                         "h2d_bytes_per_step": int(world * wl.x.numel() * 2),
+                         "d2h_bytes_per_step": int(wl.V * 4 + 4), "ms_per_step": e_ms}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(wl)
+    if wl.comm is not None:
+        _mom.nccl_comm_destroy(wl.comm)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """Reference arm: the CPU oracle (this paper-only tier's baseline) on the host cores."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # rank 0 alone runs and prints; the others exit 0 without work
+    import oracle
+    cfg = synth.CONFIGS[args.config]
+    d, I, S, C = cfg.hidden, cfg.intermediate, cfg.S, cfg.C
+    threads = oracle.default_threads()
+    wg, wu, wd = synth.mlp_weights(d, I, 0, "cpu", torch.bfloat16)
+    # rows of the workload's input (the same seeded generator as the GPU arm's rank 0)
+    xs = synth.hidden(S, d, "cpu", torch.bfloat16) if S * d <= (1 << 28) else None
+    if xs is None:
+        raise SystemExit("workload too large for the host reference")
+    wg32, wu32, wd32 = wg.float().numpy(), wu.float().numpy(), wd.float().numpy()
+    rows_per_step = threads
+    steps_rows = synth.sample_rows(S, C, n_random=rows_per_step * (args.steps + args.warmup))
+    x32 = xs.float().numpy()
+    times = []
+    for s in range(args.warmup + args.steps):
+        rows = steps_rows[(s * rows_per_step) % max(1, len(steps_rows) - rows_per_step):][:rows_per_step]
+        t0 = time.perf_counter()
+        oracle.mlp_rows(x32, x32, wg32, wu32, wd32, rows, nthreads=threads)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    step_s = statistics.mean(times)
+    value = rows_per_step / step_s
+    res = {"impl": "reference", "metric": "prefill MLP tokens/s (MOM mini-sequence path: KV offload + M-chunk SwiGLU MLP + last-token MLP/LM head/argmax + KV reload)",
+           "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic (seeded, synth/)",
+           "config": {"workload": cfg.name, "hidden": d, "intermediate": I, "seq_len_per_gpu": S, "minseq_len": C},
+           "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+                            "sample": f"{rows_per_step} sampled rows per step of the layer-0 MLP (float64 C oracle)"},
+           "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(res), flush=True)
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_mine(args)
+
+
+if __name__ == "__main__":
+    main()

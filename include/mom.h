@@ -1,0 +1,189 @@
+/*
+ * mom.h -- C ABI of libmom.so, the B200 (sm_100a) hot path of MOM:
+ * "Memory-efficient Offloaded Mini-sequence Inference" (arXiv 2504.12526).
+ *
+ * Citations: "P:<n>" = line n of the paper text (reference PAPER.md), with its section /
+ * algorithm / equation; "S:<n>" = line n of the reference SPEC.md (interfaces only).
+ *
+ * The path (Alg. 1), per transformer layer, after attention (unchanged):
+ *   - offload the layer's K/V to host memory                 -> mom_kv_offload
+ *   - non-final layers: partition the MLP input A into M = ceil(S/C) mini-sequences and
+ *     compute O_i = MLP(A_i), O = concat(O_i)                 -> mom_mlp_minseq_fwd
+ *   - final layer: A_last = A[:, -1, :], O_last = MLP(A_last) -> mom_mlp_last_token
+ *     L = LM_Head(O_last), greedy token = argmax L           -> mom_lm_head_last
+ *     transfer the offloaded cache back to the GPU            -> mom_kv_reload
+ *   - token-sharded multi-GPU: gather every rank's MLP rows   -> mom_allgather_rows
+ *
+ * MLP is the Llama SwiGLU MLP: MLP(A) = (Swish(A W_gate) (.) A W_up) W_down,
+ * Swish(z) = z * sigmoid(z).  Weights are in nn.Linear layout (row-major):
+ *   W_gate, W_up: [intermediate, hidden];  W_down: [hidden, intermediate];  W_head: [vocab, hidden].
+ * Activations are row-major [rows, hidden] with B = 1 ("we assume B = 1").
+ *
+ * Conventions (all entry points):
+ *   Ownership   The caller allocates every buffer (device memory, pinned host memory,
+ *               workspace, streams, events).  The library allocates no memory, keeps no
+ *               per-call state, and never synchronises the host.
+ *   Async       Compute calls enqueue kernels on `stream` and return.  Kernel faults surface
+ *               at the caller's next synchronisation (as with cuBLAS).
+ *   Errors      A non-OK status means NOTHING was enqueued (argument errors are detected
+ *               before any launch); mom_last_error() returns a thread-local message.
+ *   Alignment   Device pointers must be 16-byte aligned and row pitches (hidden*w,
+ *               intermediate*w, w = element bytes) multiples of 16 bytes (TMA rule).
+ *   Dtypes      MOM_BF16: bf16 storage, fp32 accumulation, fp32 SiLU, one RNE rounding of
+ *               the [C, I] intermediate and one of each output (tcgen05 tensor-core path).
+ *               MOM_F32: fp32 storage and arithmetic (SIMT path, small parity configs).
+ *   Threads     Thread-safe; the only mutable globals are the thread-local error string and
+ *               once-initialised per-device caches (SM count, driver entry point).
+ *   Streams     mom_stream_t / mom_event_t are cudaStream_t / cudaEvent_t passed as void*.
+ */
+#ifndef MOM_H_
+#define MOM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MOM_OK = 0,
+  MOM_ERR_INVALID_ARG = 1,  /* null pointer, size < 1, misalignment, bad aliasing, non-pinned host */
+  MOM_ERR_UNSUPPORTED = 2,  /* valid arguments this build does not implement (e.g. dtype/shape) */
+  MOM_ERR_WORKSPACE = 3,    /* workspace smaller than the matching *_workspace_bytes() query   */
+  MOM_ERR_CUDA = 4,         /* a CUDA runtime/driver call failed while enqueueing              */
+  MOM_ERR_NCCL = 5          /* NCCL missing or an NCCL call failed                            */
+} mom_status_t;
+
+typedef enum { MOM_BF16 = 0, MOM_F32 = 1 } mom_dtype_t;
+
+typedef void *mom_stream_t; /* cudaStream_t (NULL = legacy default stream) */
+typedef void *mom_event_t;  /* cudaEvent_t, caller-created                 */
+
+/* Thread-local description of the last non-OK status returned on this thread ("" if none). */
+const char *mom_last_error(void);
+/* Library version / build string (arch, kernel variants). */
+const char *mom_version(void);
+
+/* ------------------------------------------------------------------------------------
+ * a1. Mini-sequence plan (host only).  Alg. 1: "Partition A into M = ceil(S/C)
+ * mini-sequences {A_i}, where each A_i in R^{B x N x d} and N ~= C"; sizes
+ * (C, ..., C, S-(M-1)C).  Writes min(M, cap) (start, length) pairs into
+ * starts/lens (either may be NULL when cap == 0) and returns M, or -1 if S < 1 or C < 1.
+ * ---------------------------------------------------------------------------------- */
+int64_t mom_plan_minseq(int64_t S, int64_t minseq_len, int64_t *starts, int64_t *lens, int64_t cap);
+
+/* ------------------------------------------------------------------------------------
+ * a2-a4. Mini-sequence SwiGLU MLP over S tokens.  Alg. 1 P:109-113 with MLP per P:144:
+ *   for i = 1..M:  H_i = Swish(A_i W_gate^T) (.) (A_i W_up^T)     [C_i, I]   (Phase A)
+ *                  O_i = R_i + H_i W_down^T                        [C_i, d]   (Phase B)
+ *   O = concat(O_1..O_M): each O_i is written at its rows of `out` (no concat copy).
+ * The [S, I] intermediate of Eq. 1 never exists: only one mini-sequence's H_i
+ * lives in `workspace` at a time, so the transient is C*I*w bytes (Eq. 3).
+ *
+ *   x          device [S, hidden]         MLP input A (the post-attention-norm hidden states)
+ *   residual   device [S, hidden] or NULL NULL => out = MLP(x) exactly as Alg. 1's O_i;
+ *                                         else out = residual + MLP(x) (fused, fp32 add)
+ *   w_gate     device [intermediate, hidden]
+ *   w_up       device [intermediate, hidden]
+ *   w_down     device [hidden, intermediate]
+ *   out        device [S, hidden]         may equal residual and/or x (in place); must not
+ *                                         partially overlap either
+ *   S, hidden, intermediate >= 1; minseq_len = C >= 1 (C >= S gives M = 1)
+ *   workspace  device, >= mom_mlp_minseq_workspace_bytes(S, hidden, intermediate, C, dt)
+ * Outputs are bitwise identical for every C (no split-K, no atomics, C-independent tiles).
+ * ---------------------------------------------------------------------------------- */
+size_t mom_mlp_minseq_workspace_bytes(int64_t S, int64_t hidden, int64_t intermediate,
+                                      int64_t minseq_len, mom_dtype_t dt);
+mom_status_t mom_mlp_minseq_fwd(const void *x, const void *residual, const void *w_gate,
+                                const void *w_up, const void *w_down, void *out, int64_t S,
+                                int64_t hidden, int64_t intermediate, int64_t minseq_len,
+                                mom_dtype_t dt, void *workspace, size_t workspace_bytes,
+                                mom_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * a6. Final layer on the last token only.  Alg. 1: A_last = A[:, -1, :]
+ * (pass x + (S-1)*hidden), O_last = MLP(A_last) (+ residual_last if non-NULL).
+ * HBM-bound GEMV pair: h = Swish(W_gate x) (.) (W_up x) kept in fp32 in `workspace`, then
+ * out_last = residual_last + W_down h rounded once to dt.
+ *   x_last, residual_last (or NULL), out_last: device [hidden]; weights as above.
+ *   workspace >= mom_mlp_last_token_workspace_bytes(intermediate).
+ * ---------------------------------------------------------------------------------- */
+size_t mom_mlp_last_token_workspace_bytes(int64_t intermediate);
+mom_status_t mom_mlp_last_token(const void *x_last, const void *residual_last, const void *w_gate,
+                                const void *w_up, const void *w_down, void *out_last,
+                                int64_t hidden, int64_t intermediate, mom_dtype_t dt,
+                                void *workspace, size_t workspace_bytes, mom_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * a7-a8. LM head on the last token + greedy token.  Alg. 1 P:105 "L = LM_Head(O_last)";
+ * the head's intermediate is V.  Optional final RMSNorm prologue (applied
+ * after slicing): hn = h / sqrt(mean(h^2) + eps) (.) norm_gain.
+ *   h_last     device [hidden] (dtype dt)
+ *   norm_gain  device [hidden] (dtype dt) or NULL (no norm; eps ignored)
+ *   w_head     device [vocab, hidden] (dtype dt)
+ *   logits     device [vocab] fp32, or NULL (not stored)
+ *   argmax     device int32[1]: index of the max logit, ties -> lowest index
+ *   workspace  >= mom_lm_head_workspace_bytes(vocab)
+ * ---------------------------------------------------------------------------------- */
+size_t mom_lm_head_workspace_bytes(int64_t vocab);
+mom_status_t mom_lm_head_last(const void *h_last, const void *norm_gain, float eps,
+                              const void *w_head, float *logits, int32_t *argmax, int64_t hidden,
+                              int64_t vocab, mom_dtype_t dt, void *workspace,
+                              size_t workspace_bytes, mom_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * a9. KV offload.  Alg. 1 P:99 "Update and offload KV cache to CPU"; sec. 3.2 P:127.
+ * Records an event on producer_stream, makes copy_stream wait on it, enqueues one
+ * cudaMemcpyAsync device->host of `bytes` on copy_stream, then records `done` on
+ * copy_stream.  The copy overlaps whatever producer_stream runs next (the MLP).  The
+ * caller must not rewrite or free kv_dev before `done` completes.
+ *   kv_dev          device, 16-B aligned      kv_host_pinned  page-locked host (checked)
+ *   done            caller-created event (may be NULL)
+ * a10. KV reload.  Alg. 1 P:106 "Transfer offloaded cache back to GPU for decode stage":
+ * one cudaMemcpyAsync host->device on copy_stream, then records `done` (may be NULL).
+ * Both: bytes >= 1.  Round trip is bytewise exact.
+ * ---------------------------------------------------------------------------------- */
+mom_status_t mom_kv_offload(const void *kv_dev, void *kv_host_pinned, size_t bytes,
+                            mom_stream_t producer_stream, mom_stream_t copy_stream,
+                            mom_event_t done);
+mom_status_t mom_kv_reload(const void *kv_host_pinned, void *kv_dev, size_t bytes,
+                           mom_stream_t copy_stream, mom_event_t done);
+
+/* ------------------------------------------------------------------------------------
+ * a11. Token-sharded multi-GPU (one process per GPU).  The S tokens are split into
+ * contiguous row ranges per rank; the position-wise MLP needs no exchange, and one
+ * in-place all-gather per layer rebuilds the [S, hidden] rows the next (unchanged,
+ * P:81) attention layer needs.  NCCL is loaded at run time (dlopen libnccl.so.2).
+ *   mom_nccl_get_unique_id   rank 0 writes the 128-byte NCCL unique id to id_out
+ *   mom_nccl_comm_init       every rank: *comm_out = ncclCommInitRank(nranks, id, rank)
+ *                            (the current CUDA device must already be set)
+ *   mom_nccl_comm_destroy    ncclCommDestroy
+ *   mom_allgather_rows       rows: device [nranks * rows_per_rank, hidden]; this rank's
+ *                            shard is at row rank*rows_per_rank; in-place ncclAllGather on
+ *                            `stream`; after completion every rank holds all rows.
+ * ---------------------------------------------------------------------------------- */
+mom_status_t mom_nccl_get_unique_id(void *id_out /* 128 bytes */);
+mom_status_t mom_nccl_comm_init(void **comm_out, int nranks, const void *id /* 128 B */, int rank);
+mom_status_t mom_nccl_comm_destroy(void *comm);
+mom_status_t mom_allgather_rows(void *rows, int64_t rows_per_rank, int64_t hidden, mom_dtype_t dt,
+                                void *comm, int rank, int nranks, mom_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * Instrumentation (used by bench.py for the per-kernel roofline; not part of the path).
+ * While enabled on the calling thread, every kernel launch issued by the compute entry
+ * points is bracketed by cudaEventRecord(events[2j]) / cudaEventRecord(events[2j+1]) on its
+ * stream, kinds[j] is set to the launch kind and *count is incremented (j = *count before
+ * the launch; launches beyond `capacity` pairs are not recorded).  Kinds:
+ *   0 phase A tcgen05 (gate/up + SiLU*mul)   1 phase B tcgen05 (down + residual)
+ *   2 phase A fp32 SIMT                      3 phase B fp32 SIMT
+ *   4 last-token GEMV pair                   5 LM head GEMV + argmax
+ * events: caller-created cudaEvent_t array of 2*capacity; kinds: int32[capacity];
+ * count: host int64.  Pass events == NULL to disable.  Thread-local, host-side only.
+ * ---------------------------------------------------------------------------------- */
+mom_status_t mom_set_timing_events(mom_event_t *events, int32_t *kinds, int64_t capacity, int64_t *count);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+#endif /* MOM_H_ */

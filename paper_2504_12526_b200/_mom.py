@@ -1,0 +1,239 @@
+"""Thin ctypes binding of libmom.so (include/mom.h).  Argument marshalling only: every step
+of the path runs in the library's CUDA kernels; torch supplies device memory, pinned host
+memory and streams.  There is no fallback: if libmom.so is missing or a call fails, an
+exception is raised."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libmom.so")
+
+MOM_OK, MOM_ERR_INVALID_ARG, MOM_ERR_UNSUPPORTED, MOM_ERR_WORKSPACE, MOM_ERR_CUDA, MOM_ERR_NCCL = range(6)
+MOM_BF16, MOM_F32 = 0, 1
+STATUS_NAMES = {0: "MOM_OK", 1: "MOM_ERR_INVALID_ARG", 2: "MOM_ERR_UNSUPPORTED", 3: "MOM_ERR_WORKSPACE",
+                4: "MOM_ERR_CUDA", 5: "MOM_ERR_NCCL"}
+
+# name -> (restype, argtypes); the symbol table checked by tests/test_abi.py against include/mom.h
+_p, _i64, _i32, _sz, _f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t, ctypes.c_float
+SIGNATURES = {
+    "mom_last_error": (ctypes.c_char_p, []),
+    "mom_version": (ctypes.c_char_p, []),
+    "mom_plan_minseq": (_i64, [_i64, _i64, _p, _p, _i64]),
+    "mom_mlp_minseq_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64, _i32]),
+    "mom_mlp_minseq_fwd": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i32, _p, _sz, _p]),
+    "mom_mlp_last_token_workspace_bytes": (_sz, [_i64]),
+    "mom_mlp_last_token": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _p, _sz, _p]),
+    "mom_lm_head_workspace_bytes": (_sz, [_i64]),
+    "mom_lm_head_last": (_i32, [_p, _p, _f32, _p, _p, _p, _i64, _i64, _i32, _p, _sz, _p]),
+    "mom_kv_offload": (_i32, [_p, _p, _sz, _p, _p, _p]),
+    "mom_kv_reload": (_i32, [_p, _p, _sz, _p, _p]),
+    "mom_nccl_get_unique_id": (_i32, [_p]),
+    "mom_nccl_comm_init": (_i32, [ctypes.POINTER(ctypes.c_void_p), _i32, _p, _i32]),
+    "mom_nccl_comm_destroy": (_i32, [_p]),
+    "mom_allgather_rows": (_i32, [_p, _i64, _i64, _i32, _p, _i32, _i32, _p]),
+    "mom_set_timing_events": (_i32, [_p, _p, _i64, _p]),
+}
+
+KIND_NAMES = {0: "phaseA_tc", 1: "phaseB_tc", 2: "phaseA_f32", 3: "phaseB_f32", 4: "last_token_gemv",
+              5: "lm_head_gemv"}
+
+
+class LaunchTimer:
+    """Per-launch CUDA-event timing of the library's kernels (mom_set_timing_events).
+    Events are recorded by the library on the stream each kernel is launched on."""
+
+    def __init__(self, capacity: int):
+        self.capacity = capacity
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(2 * capacity)]
+        for e in self.events:  # force creation of the underlying cudaEvent_t
+            e.record()
+        torch.cuda.synchronize()
+        self._handles = (ctypes.c_void_p * (2 * capacity))(*[e.cuda_event for e in self.events])
+        self._kinds = (ctypes.c_int32 * capacity)()
+        self._count = ctypes.c_int64(0)
+
+    def __enter__(self):
+        self._count.value = 0
+        _check(lib().mom_set_timing_events(self._handles, self._kinds, self.capacity, ctypes.byref(self._count)))
+        return self
+
+    def __exit__(self, *exc):
+        lib().mom_set_timing_events(None, None, 0, None)
+        return False
+
+    def results(self):
+        """[(kind_name, ms)] for every recorded launch (call after synchronising)."""
+        out = []
+        for j in range(min(self._count.value, self.capacity)):
+            out.append((KIND_NAMES.get(self._kinds[j], str(self._kinds[j])),
+                        self.events[2 * j].elapsed_time(self.events[2 * j + 1])))
+        return out
+
+_lib = None
+
+
+class MomError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def lib():
+    """Load libmom.so (raises if it was not built -- there is no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2504_12526_b200.build` "
+                              "or __graft_entry__.build()")
+        l = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(l, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = l
+    return _lib
+
+
+def _check(status: int):
+    if status != MOM_OK:
+        raise MomError(status, lib().mom_last_error().decode(errors="replace"))
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return MOM_BF16
+    if t.dtype == torch.float32:
+        return MOM_F32
+    raise TypeError(f"unsupported dtype {t.dtype} (bf16 or fp32)")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _event_handle(done):
+    if done is None:
+        return None
+    return done.cuda_event or None
+
+
+def version() -> str:
+    return lib().mom_version().decode()
+
+
+def plan_minseq(S: int, minseq_len: int):
+    """Alg. 1: [(start, length)] of the M = ceil(S/C) mini-sequences (host only)."""
+    M = lib().mom_plan_minseq(S, minseq_len, None, None, 0)
+    if M < 0:
+        raise ValueError("S and minseq_len must be >= 1")
+    starts = (ctypes.c_int64 * M)()
+    lens = (ctypes.c_int64 * M)()
+    lib().mom_plan_minseq(S, minseq_len, starts, lens, M)
+    return [(starts[i], lens[i]) for i in range(M)]
+
+
+def mlp_minseq_workspace_bytes(S: int, hidden: int, intermediate: int, minseq_len: int, dtype) -> int:
+    dt = MOM_BF16 if dtype == torch.bfloat16 else MOM_F32
+    return int(lib().mom_mlp_minseq_workspace_bytes(S, hidden, intermediate, minseq_len, dt))
+
+
+def mlp_minseq_fwd(x, residual, w_gate, w_up, w_down, out, minseq_len: int, workspace=None, stream=None):
+    """Alg. 1: out = residual + concat_i MLP(x_i) over M = ceil(S/C) mini-sequences."""
+    S, hidden = x.shape
+    I = w_gate.shape[0]
+    dt = _dt(x)
+    if workspace is None:
+        nbytes = lib().mom_mlp_minseq_workspace_bytes(S, hidden, I, minseq_len, dt)
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    ws_bytes = workspace.numel() * workspace.element_size()
+    _check(lib().mom_mlp_minseq_fwd(_ptr(x), _ptr(residual), _ptr(w_gate), _ptr(w_up), _ptr(w_down), _ptr(out),
+                                    S, hidden, I, minseq_len, dt, _ptr(workspace), ws_bytes, _stream(stream)))
+    return out
+
+
+def mlp_last_token(x_last, residual_last, w_gate, w_up, w_down, out_last, workspace=None, stream=None):
+    """Alg. 1: O_last = residual_last + MLP(A_last) on one token (GEMV pair)."""
+    hidden = x_last.shape[-1]
+    I = w_gate.shape[0]
+    dt = _dt(x_last)
+    if workspace is None:
+        workspace = torch.empty(lib().mom_mlp_last_token_workspace_bytes(I), dtype=torch.uint8, device=x_last.device)
+    _check(lib().mom_mlp_last_token(_ptr(x_last), _ptr(residual_last), _ptr(w_gate), _ptr(w_up), _ptr(w_down),
+                                    _ptr(out_last), hidden, I, dt, _ptr(workspace),
+                                    workspace.numel() * workspace.element_size(), _stream(stream)))
+    return out_last
+
+
+def lm_head_last(h_last, norm_gain, eps: float, w_head, logits, argmax, workspace=None, stream=None):
+    """Alg. 1: logits = W_head . rmsnorm(h_last) (fp32) and argmax (int32, ties -> lowest)."""
+    hidden = h_last.shape[-1]
+    V = w_head.shape[0]
+    dt = _dt(h_last)
+    if workspace is None:
+        workspace = torch.empty(lib().mom_lm_head_workspace_bytes(V), dtype=torch.uint8, device=h_last.device)
+    _check(lib().mom_lm_head_last(_ptr(h_last), _ptr(norm_gain), float(eps), _ptr(w_head), _ptr(logits),
+                                  _ptr(argmax), hidden, V, dt, _ptr(workspace),
+                                  workspace.numel() * workspace.element_size(), _stream(stream)))
+    return argmax
+
+
+def kv_offload(kv_dev, kv_host_pinned, producer_stream=None, copy_stream=None, done=None, nbytes=None):
+    """Alg. 1: async D2H of one layer's K/V into pinned host memory on copy_stream."""
+    n = nbytes if nbytes is not None else kv_dev.numel() * kv_dev.element_size()
+    ev = _event_handle(done)
+    _check(lib().mom_kv_offload(_ptr(kv_dev), _ptr(kv_host_pinned), n, _stream(producer_stream),
+                                _stream(copy_stream), ev))
+    if done is not None and ev is None:  # torch creates its event lazily: record after the copy
+        done.record(copy_stream if copy_stream is not None else torch.cuda.current_stream())
+    return done
+
+
+def kv_reload(kv_host_pinned, kv_dev, copy_stream=None, done=None, nbytes=None):
+    """Alg. 1: async H2D of the offloaded cache before decode."""
+    n = nbytes if nbytes is not None else kv_dev.numel() * kv_dev.element_size()
+    ev = _event_handle(done)
+    _check(lib().mom_kv_reload(_ptr(kv_host_pinned), _ptr(kv_dev), n, _stream(copy_stream), ev))
+    if done is not None and ev is None:
+        done.record(copy_stream if copy_stream is not None else torch.cuda.current_stream())
+    return done
+
+
+def nccl_get_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().mom_nccl_get_unique_id(buf))
+    return bytes(buf)
+
+
+def nccl_comm_init(nranks: int, uid: bytes, rank: int) -> int:
+    comm = ctypes.c_void_p()
+    buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    _check(lib().mom_nccl_comm_init(ctypes.byref(comm), nranks, buf, rank))
+    return comm.value
+
+
+def nccl_comm_destroy(comm: int):
+    _check(lib().mom_nccl_comm_destroy(comm))
+
+
+def allgather_rows(rows, rows_per_rank: int, comm: int, rank: int, nranks: int, stream=None):
+    """In-place all-gather of every rank's [rows_per_rank, hidden] shard of `rows`."""
+    hidden = rows.shape[-1]
+    _check(lib().mom_allgather_rows(_ptr(rows), rows_per_rank, hidden, _dt(rows), comm, rank, nranks,
+                                    _stream(stream)))
+    return rows

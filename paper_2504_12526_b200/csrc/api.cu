@@ -1,0 +1,505 @@
+// api.cu -- the C ABI of libmom.so (include/mom.h): argument validation, mini-sequence
+// planning (Alg. 1), TMA descriptor encoding, kernel launches, KV offload/reload
+// (sec. 3.2) and the NCCL all-gather for token-sharded runs.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/mom.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+mom_status_t fail(mom_status_t st, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+mom_status_t cuda_fail(cudaError_t e, const char *what) {
+  return fail(MOM_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+size_t dtype_bytes(mom_dtype_t dt) { return dt == MOM_BF16 ? 2 : 4; }
+
+bool valid_dtype(mom_dtype_t dt) { return dt == MOM_BF16 || dt == MOM_F32; }
+
+// [a, a+na) and [b, b+nb) overlap but are not identical
+bool partial_overlap(const void *a, size_t na, const void *b, size_t nb) {
+  if (!a || !b) return false;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+  if (a0 == b0) return false;
+  return a0 < b0 + nb && b0 < a0 + na;
+}
+
+// ---- per-device cache: SM count (B200: 148) ----
+int num_sms_current(int *out) {
+  static std::mutex mu;
+  static int cache[64];
+  static bool have[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && have[dev]) {
+    *out = cache[dev];
+    return 0;
+  }
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  if (dev < 64) {
+    cache[dev] = n;
+    have[dev] = true;
+  }
+  *out = n;
+  return 0;
+}
+
+// ---- cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda) ----
+using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                              const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+  static std::once_flag once;
+  static EncodeFn fn = nullptr;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 2D bf16 row-major [rows, cols] tensor, box = 64 columns (128 B, one 128-B swizzle span) x 128 rows.
+mom_status_t make_tmap(CUtensorMap *m, const void *base, uint64_t rows, uint64_t cols, const char *what) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return fail(MOM_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(MOM_ERR_CUDA, "cuTensorMapEncodeTiled(%s) failed: %d", what, (int)r);
+  return MOM_OK;
+}
+
+// ---- per-thread launch timing hook (mom_set_timing_events) ----
+struct TimingHook {
+  cudaEvent_t *ev = nullptr;
+  int32_t *kinds = nullptr;
+  int64_t cap = 0;
+  int64_t *count = nullptr;
+};
+thread_local TimingHook g_hook;
+
+struct ScopedTiming {
+  cudaStream_t s;
+  int64_t slot = -1;
+  ScopedTiming(cudaStream_t stream, int kind) : s(stream) {
+    if (g_hook.ev && g_hook.count && *g_hook.count < g_hook.cap) {
+      slot = (*g_hook.count)++;
+      g_hook.kinds[slot] = kind;
+      cudaEventRecord(g_hook.ev[2 * slot], s);
+    }
+  }
+  ~ScopedTiming() {
+    if (slot >= 0) cudaEventRecord(g_hook.ev[2 * slot + 1], s);
+  }
+};
+
+int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *mom_last_error(void) { return g_err; }
+
+mom_status_t mom_set_timing_events(mom_event_t *events, int32_t *kinds, int64_t capacity, int64_t *count) {
+  g_err[0] = 0;
+  if (!events) {
+    g_hook = TimingHook{};
+    return MOM_OK;
+  }
+  if (!kinds || !count || capacity < 1) return fail(MOM_ERR_INVALID_ARG, "mom_set_timing_events: bad arguments");
+  g_hook.ev = reinterpret_cast<cudaEvent_t *>(events);
+  g_hook.kinds = kinds;
+  g_hook.cap = capacity;
+  g_hook.count = count;
+  return MOM_OK;
+}
+
+const char *mom_version(void) {
+  return "libmom 0.1 sm_100a: tcgen05 dual-B GEMM (cta_group 1|2), SIMT f32, GEMV, KV copy, NCCL allgather";
+}
+
+int64_t mom_plan_minseq(int64_t S, int64_t C, int64_t *starts, int64_t *lens, int64_t cap) {
+  if (S < 1 || C < 1) return -1;
+  const int64_t M = (S + C - 1) / C;  // Alg. 1: M = ceil(S/C)
+  for (int64_t i = 0; i < M && i < cap; ++i) {
+    const int64_t r0 = i * C;
+    const int64_t r1 = (r0 + C < S) ? r0 + C : S;
+    if (starts) starts[i] = r0;
+    if (lens) lens[i] = r1 - r0;
+  }
+  return M;
+}
+
+size_t mom_mlp_minseq_workspace_bytes(int64_t S, int64_t hidden, int64_t intermediate, int64_t C,
+                                      mom_dtype_t dt) {
+  (void)hidden;
+  if (S < 1 || intermediate < 1 || C < 1 || !valid_dtype(dt)) return 0;
+  const int64_t rows = C < S ? C : S;  // one mini-sequence's H_i: C * I elements (Eq. 3)
+  const size_t b = static_cast<size_t>(rows) * static_cast<size_t>(intermediate) * dtype_bytes(dt);
+  return (b + 255) & ~static_cast<size_t>(255);
+}
+
+mom_status_t mom_mlp_minseq_fwd(const void *x, const void *residual, const void *w_gate, const void *w_up,
+                                const void *w_down, void *out, int64_t S, int64_t hidden, int64_t intermediate,
+                                int64_t C, mom_dtype_t dt, void *workspace, size_t workspace_bytes,
+                                mom_stream_t stream_) {
+  g_err[0] = 0;
+  if (!x || !w_gate || !w_up || !w_down || !out || !workspace)
+    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd: null pointer");
+  if (S < 1 || hidden < 1 || intermediate < 1 || C < 1)
+    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd: S, hidden, intermediate, minseq_len must be >= 1");
+  if (!valid_dtype(dt)) return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd: bad dtype %d", (int)dt);
+  const size_t w = dtype_bytes(dt);
+  if ((hidden * w) % 16 || (intermediate * w) % 16)
+    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd: row pitch must be a multiple of 16 bytes");
+  if (!aligned16(x) || !aligned16(residual) || !aligned16(w_gate) || !aligned16(w_up) || !aligned16(w_down) ||
+      !aligned16(out) || !aligned16(workspace))
+    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd: pointers must be 16-byte aligned");
+  if (S > INT32_MAX || hidden > INT32_MAX || intermediate > INT32_MAX)
+    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd: dimension exceeds int32");
+  const size_t act_bytes = static_cast<size_t>(S) * hidden * w;
+  if (partial_overlap(out, act_bytes, x, act_bytes) || partial_overlap(out, act_bytes, residual, act_bytes))
+    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd: out partially overlaps x or residual");
+  const size_t need = mom_mlp_minseq_workspace_bytes(S, hidden, intermediate, C, dt);
+  if (workspace_bytes < need)
+    return fail(MOM_ERR_WORKSPACE, "mom_mlp_minseq_fwd: workspace %zu < required %zu bytes", workspace_bytes, need);
+
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  int num_sms = 0;
+  if (num_sms_current(&num_sms) != 0) return fail(MOM_ERR_CUDA, "mom_mlp_minseq_fwd: no CUDA device");
+  const int64_t M = (S + C - 1) / C;  // Alg. 1
+
+  if (dt == MOM_F32) {
+    for (int64_t i = 0; i < M; ++i) {  // Alg. 1: for i = 1..M
+      const int64_t r0 = i * C;
+      const int64_t rows = (r0 + C < S) ? C : S - r0;
+      const float *xi = static_cast<const float *>(x) + r0 * hidden;
+      const float *ri = residual ? static_cast<const float *>(residual) + r0 * hidden : nullptr;
+      float *oi = static_cast<float *>(out) + r0 * hidden;  // concat: O_i lands at its rows
+      float *h = static_cast<float *>(workspace);
+      cudaError_t e;
+      {
+        ScopedTiming tm(stream, 2);
+        e = mom::launch_phase_a_f32(xi, static_cast<const float *>(w_gate),
+                                              static_cast<const float *>(w_up), h, (int)rows, (int)hidden,
+                                              (int)intermediate, stream);
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "phase A (f32)");
+      {
+        ScopedTiming tm(stream, 3);
+        e = mom::launch_phase_b_f32(h, static_cast<const float *>(w_down), ri, oi, (int)rows, (int)hidden,
+                                    (int)intermediate, stream);
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "phase B (f32)");
+    }
+    return MOM_OK;
+  }
+
+  // bf16 tcgen05 path
+  const int cta_group = env_int("MOM_CTA_GROUP", 2) == 1 ? 1 : 2;
+  const uint32_t group_a = static_cast<uint32_t>(env_int("MOM_GROUP_M_A", 0));
+  const uint32_t group_b = static_cast<uint32_t>(env_int("MOM_GROUP_M_B", 0));
+  CUtensorMap tm_wg, tm_wu, tm_wd;
+  mom_status_t st;
+  if ((st = make_tmap(&tm_wg, w_gate, intermediate, hidden, "w_gate")) != MOM_OK) return st;
+  if ((st = make_tmap(&tm_wu, w_up, intermediate, hidden, "w_up")) != MOM_OK) return st;
+  if ((st = make_tmap(&tm_wd, w_down, hidden, intermediate, "w_down")) != MOM_OK) return st;
+  for (int64_t i = 0; i < M; ++i) {  // Alg. 1: for i = 1..M (sequential on `stream`)
+    const int64_t r0 = i * C;
+    const int64_t rows = (r0 + C < S) ? C : S - r0;
+    const __nv_bfloat16 *xi = static_cast<const __nv_bfloat16 *>(x) + r0 * hidden;
+    const __nv_bfloat16 *ri = residual ? static_cast<const __nv_bfloat16 *>(residual) + r0 * hidden : nullptr;
+    __nv_bfloat16 *oi = static_cast<__nv_bfloat16 *>(out) + r0 * hidden;
+    __nv_bfloat16 *h = static_cast<__nv_bfloat16 *>(workspace);
+    // Per-mini-sequence maps: the row bound is C_i, so TMA zero-fills loads past the end of
+    // this mini-sequence and no tile reads another mini-sequence's rows.
+    CUtensorMap tm_x, tm_h;
+    if ((st = make_tmap(&tm_x, xi, rows, hidden, "x_i")) != MOM_OK) return st;
+    if ((st = make_tmap(&tm_h, h, rows, intermediate, "h_i")) != MOM_OK) return st;
+    mom::TcPhaseArgs a{};
+    a.tm_a = &tm_x; a.tm_b0 = &tm_wg; a.tm_b1 = &tm_wu;
+    a.rows = (uint32_t)rows; a.n_out = (uint32_t)intermediate; a.k = (uint32_t)hidden;
+    a.out = h; a.residual = nullptr; a.ld_out = (uint32_t)intermediate;
+    a.cta_group = cta_group; a.group_m = group_a; a.num_sms = num_sms;
+    cudaError_t e;
+    {
+      ScopedTiming tm(stream, 0);
+      e = mom::launch_phase_a_tc(a, stream);  // H_i = Swish(A_i Wg^T) (.) A_i Wu^T
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "phase A (tcgen05)");
+    mom::TcPhaseArgs b{};
+    b.tm_a = &tm_h; b.tm_b0 = &tm_wd; b.tm_b1 = &tm_wd;
+    b.rows = (uint32_t)rows; b.n_out = (uint32_t)hidden; b.k = (uint32_t)intermediate;
+    b.out = oi; b.residual = ri; b.ld_out = (uint32_t)hidden;
+    b.cta_group = cta_group; b.group_m = group_b; b.num_sms = num_sms;
+    {
+      ScopedTiming tm(stream, 1);
+      e = mom::launch_phase_b_tc(b, stream);  // O_i = R_i + H_i Wd^T, written at rows r0..
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "phase B (tcgen05)");
+  }
+  return MOM_OK;
+}
+
+size_t mom_mlp_last_token_workspace_bytes(int64_t intermediate) {
+  if (intermediate < 1) return 0;
+  return ((static_cast<size_t>(intermediate) * 4) + 255) & ~static_cast<size_t>(255);
+}
+
+mom_status_t mom_mlp_last_token(const void *x_last, const void *residual_last, const void *w_gate,
+                                const void *w_up, const void *w_down, void *out_last, int64_t hidden,
+                                int64_t intermediate, mom_dtype_t dt, void *workspace, size_t workspace_bytes,
+                                mom_stream_t stream) {
+  g_err[0] = 0;
+  if (!x_last || !w_gate || !w_up || !w_down || !out_last || !workspace)
+    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_last_token: null pointer");
+  if (hidden < 1 || intermediate < 1) return fail(MOM_ERR_INVALID_ARG, "mom_mlp_last_token: sizes must be >= 1");
+  if (!valid_dtype(dt)) return fail(MOM_ERR_INVALID_ARG, "mom_mlp_last_token: bad dtype");
+  const size_t w = dtype_bytes(dt);
+  if ((hidden * w) % 16 || (intermediate * w) % 16)
+    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_last_token: row pitch must be a multiple of 16 bytes");
+  if (!aligned16(x_last) || !aligned16(residual_last) || !aligned16(w_gate) || !aligned16(w_up) ||
+      !aligned16(w_down) || !aligned16(out_last) || !aligned16(workspace))
+    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_last_token: pointers must be 16-byte aligned");
+  if (partial_overlap(out_last, hidden * w, x_last, hidden * w) ||
+      partial_overlap(out_last, hidden * w, residual_last, hidden * w))
+    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_last_token: out_last partially overlaps an input");
+  if (x_last == out_last && residual_last != out_last)
+    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_last_token: out_last may alias x_last only when residual_last does too");
+  if (hidden > (1 << 24) || intermediate > (1 << 24))
+    return fail(MOM_ERR_UNSUPPORTED, "mom_mlp_last_token: staging buffers limit hidden/intermediate to 2^24");
+  const size_t need = mom_mlp_last_token_workspace_bytes(intermediate);
+  if (workspace_bytes < need) return fail(MOM_ERR_WORKSPACE, "mom_mlp_last_token: workspace %zu < %zu", workspace_bytes, need);
+  if (static_cast<size_t>(intermediate) * 4 > 227 * 1024 || static_cast<size_t>(hidden) * 4 > 227 * 1024)
+    return fail(MOM_ERR_UNSUPPORTED, "mom_mlp_last_token: vector does not fit in shared memory");
+  int num_sms = 0;
+  if (num_sms_current(&num_sms) != 0) return fail(MOM_ERR_CUDA, "mom_mlp_last_token: no CUDA device");
+  cudaError_t e;
+  ScopedTiming tm(static_cast<cudaStream_t>(stream), 4);
+  e = mom::launch_last_token_mlp(x_last, residual_last, w_gate, w_up, w_down, out_last,
+                                             static_cast<float *>(workspace), (int)hidden, (int)intermediate,
+                                             dt == MOM_BF16, num_sms, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "last-token MLP");
+  return MOM_OK;
+}
+
+size_t mom_lm_head_workspace_bytes(int64_t vocab) {
+  if (vocab < 1) return 0;
+  return 256 * 4 * sizeof(unsigned long long);  // per-block partial maxima (<= 4 per SM, <= 256 SMs)
+}
+
+mom_status_t mom_lm_head_last(const void *h_last, const void *norm_gain, float eps, const void *w_head,
+                              float *logits, int32_t *argmax, int64_t hidden, int64_t vocab, mom_dtype_t dt,
+                              void *workspace, size_t workspace_bytes, mom_stream_t stream) {
+  g_err[0] = 0;
+  if (!h_last || !w_head || !argmax || !workspace) return fail(MOM_ERR_INVALID_ARG, "mom_lm_head_last: null pointer");
+  if (hidden < 1 || vocab < 1) return fail(MOM_ERR_INVALID_ARG, "mom_lm_head_last: sizes must be >= 1");
+  if (!valid_dtype(dt)) return fail(MOM_ERR_INVALID_ARG, "mom_lm_head_last: bad dtype");
+  if (norm_gain && !(eps >= 0.0f)) return fail(MOM_ERR_INVALID_ARG, "mom_lm_head_last: eps must be >= 0");
+  const size_t w = dtype_bytes(dt);
+  if ((hidden * w) % 16) return fail(MOM_ERR_INVALID_ARG, "mom_lm_head_last: row pitch must be a multiple of 16 bytes");
+  if (!aligned16(h_last) || !aligned16(norm_gain) || !aligned16(w_head) || !aligned16(logits) ||
+      !aligned16(workspace) || (reinterpret_cast<uintptr_t>(argmax) & 3))
+    return fail(MOM_ERR_INVALID_ARG, "mom_lm_head_last: misaligned pointer");
+  if (vocab > INT32_MAX - 1) return fail(MOM_ERR_INVALID_ARG, "mom_lm_head_last: vocab exceeds int32");
+  if (static_cast<size_t>(hidden) * 4 > 200 * 1024)
+    return fail(MOM_ERR_UNSUPPORTED, "mom_lm_head_last: hidden too large for shared-memory staging");
+  const size_t need = mom_lm_head_workspace_bytes(vocab);
+  if (workspace_bytes < need) return fail(MOM_ERR_WORKSPACE, "mom_lm_head_last: workspace %zu < %zu", workspace_bytes, need);
+  int num_sms = 0;
+  if (num_sms_current(&num_sms) != 0) return fail(MOM_ERR_CUDA, "mom_lm_head_last: no CUDA device");
+  if (num_sms > 256) num_sms = 256;
+  cudaError_t e;
+  ScopedTiming tm(static_cast<cudaStream_t>(stream), 5);
+  e = mom::launch_lm_head(h_last, norm_gain, eps, w_head, logits, argmax,
+                                      static_cast<unsigned long long *>(workspace), (int)hidden, (int)vocab,
+                                      dt == MOM_BF16, num_sms, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "lm head");
+  return MOM_OK;
+}
+
+static mom_status_t check_pinned(const void *host, const char *who) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, host);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(MOM_ERR_INVALID_ARG, "%s: cannot query host pointer (%s)", who, cudaGetErrorName(e));
+  }
+  if (at.type != cudaMemoryTypeHost)
+    return fail(MOM_ERR_INVALID_ARG, "%s: host buffer is not page-locked (cudaHostAlloc / pin_memory)", who);
+  return MOM_OK;
+}
+
+mom_status_t mom_kv_offload(const void *kv_dev, void *kv_host_pinned, size_t bytes, mom_stream_t producer_stream,
+                            mom_stream_t copy_stream, mom_event_t done) {
+  g_err[0] = 0;
+  if (!kv_dev || !kv_host_pinned || bytes < 1) return fail(MOM_ERR_INVALID_ARG, "mom_kv_offload: null pointer or zero bytes");
+  if (!aligned16(kv_dev)) return fail(MOM_ERR_INVALID_ARG, "mom_kv_offload: kv_dev must be 16-byte aligned");
+  mom_status_t st = check_pinned(kv_host_pinned, "mom_kv_offload");
+  if (st != MOM_OK) return st;
+  cudaStream_t prod = static_cast<cudaStream_t>(producer_stream), cp = static_cast<cudaStream_t>(copy_stream);
+  if (prod != cp) {
+    cudaEvent_t ready;
+    cudaError_t e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "mom_kv_offload: event create");
+    e = cudaEventRecord(ready, prod);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cp, ready, 0);
+    cudaEventDestroy(ready);  // released once the recorded work completes
+    if (e != cudaSuccess) return cuda_fail(e, "mom_kv_offload: stream ordering");
+  }
+  cudaError_t e = cudaMemcpyAsync(kv_host_pinned, kv_dev, bytes, cudaMemcpyDeviceToHost, cp);
+  if (e != cudaSuccess) return cuda_fail(e, "mom_kv_offload: cudaMemcpyAsync D2H");
+  if (done) {
+    e = cudaEventRecord(static_cast<cudaEvent_t>(done), cp);
+    if (e != cudaSuccess) return cuda_fail(e, "mom_kv_offload: event record");
+  }
+  return MOM_OK;
+}
+
+mom_status_t mom_kv_reload(const void *kv_host_pinned, void *kv_dev, size_t bytes, mom_stream_t copy_stream,
+                           mom_event_t done) {
+  g_err[0] = 0;
+  if (!kv_dev || !kv_host_pinned || bytes < 1) return fail(MOM_ERR_INVALID_ARG, "mom_kv_reload: null pointer or zero bytes");
+  if (!aligned16(kv_dev)) return fail(MOM_ERR_INVALID_ARG, "mom_kv_reload: kv_dev must be 16-byte aligned");
+  mom_status_t st = check_pinned(kv_host_pinned, "mom_kv_reload");
+  if (st != MOM_OK) return st;
+  cudaStream_t cp = static_cast<cudaStream_t>(copy_stream);
+  cudaError_t e = cudaMemcpyAsync(kv_dev, kv_host_pinned, bytes, cudaMemcpyHostToDevice, cp);
+  if (e != cudaSuccess) return cuda_fail(e, "mom_kv_reload: cudaMemcpyAsync H2D");
+  if (done) {
+    e = cudaEventRecord(static_cast<cudaEvent_t>(done), cp);
+    if (e != cudaSuccess) return cuda_fail(e, "mom_kv_reload: event record");
+  }
+  return MOM_OK;
+}
+
+// ------------------------------------------------------------------------ NCCL (dlopen)
+namespace {
+typedef struct { char internal[128]; } nccl_uid_t;
+typedef int (*nccl_get_uid_fn)(nccl_uid_t *);
+typedef int (*nccl_init_fn)(void **, int, nccl_uid_t, int);
+typedef int (*nccl_destroy_fn)(void *);
+typedef int (*nccl_allgather_fn)(const void *, void *, size_t, int, void *, cudaStream_t);
+typedef const char *(*nccl_errstr_fn)(int);
+struct Nccl {
+  bool ok = false;
+  nccl_get_uid_fn get_uid = nullptr;
+  nccl_init_fn init = nullptr;
+  nccl_destroy_fn destroy = nullptr;
+  nccl_allgather_fn allgather = nullptr;
+  nccl_errstr_fn errstr = nullptr;
+  char why[256] = "";
+};
+Nccl &nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char *path = getenv("MOM_NCCL_LIB");
+    void *h = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      snprintf(n.why, sizeof(n.why), "dlopen libnccl.so.2 failed: %s", dlerror());
+      return;
+    }
+    n.get_uid = reinterpret_cast<nccl_get_uid_fn>(dlsym(h, "ncclGetUniqueId"));
+    n.init = reinterpret_cast<nccl_init_fn>(dlsym(h, "ncclCommInitRank"));
+    n.destroy = reinterpret_cast<nccl_destroy_fn>(dlsym(h, "ncclCommDestroy"));
+    n.allgather = reinterpret_cast<nccl_allgather_fn>(dlsym(h, "ncclAllGather"));
+    n.errstr = reinterpret_cast<nccl_errstr_fn>(dlsym(h, "ncclGetErrorString"));
+    n.ok = n.get_uid && n.init && n.destroy && n.allgather;
+    if (!n.ok) snprintf(n.why, sizeof(n.why), "libnccl.so.2 lacks a required symbol");
+  });
+  return n;
+}
+mom_status_t nccl_fail(int rc, const char *what) {
+  Nccl &n = nccl();
+  return fail(MOM_ERR_NCCL, "%s: nccl error %d (%s)", what, rc, n.errstr ? n.errstr(rc) : "?");
+}
+}  // namespace
+
+mom_status_t mom_nccl_get_unique_id(void *id_out) {
+  g_err[0] = 0;
+  if (!id_out) return fail(MOM_ERR_INVALID_ARG, "mom_nccl_get_unique_id: null pointer");
+  Nccl &n = nccl();
+  if (!n.ok) return fail(MOM_ERR_NCCL, "%s", n.why);
+  nccl_uid_t uid;
+  int rc = n.get_uid(&uid);
+  if (rc != 0) return nccl_fail(rc, "ncclGetUniqueId");
+  memcpy(id_out, &uid, sizeof(uid));
+  return MOM_OK;
+}
+
+mom_status_t mom_nccl_comm_init(void **comm_out, int nranks, const void *id, int rank) {
+  g_err[0] = 0;
+  if (!comm_out || !id || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(MOM_ERR_INVALID_ARG, "mom_nccl_comm_init: bad arguments");
+  Nccl &n = nccl();
+  if (!n.ok) return fail(MOM_ERR_NCCL, "%s", n.why);
+  nccl_uid_t uid;
+  memcpy(&uid, id, sizeof(uid));
+  int rc = n.init(comm_out, nranks, uid, rank);
+  if (rc != 0) return nccl_fail(rc, "ncclCommInitRank");
+  return MOM_OK;
+}
+
+mom_status_t mom_nccl_comm_destroy(void *comm) {
+  g_err[0] = 0;
+  if (!comm) return fail(MOM_ERR_INVALID_ARG, "mom_nccl_comm_destroy: null comm");
+  Nccl &n = nccl();
+  if (!n.ok) return fail(MOM_ERR_NCCL, "%s", n.why);
+  int rc = n.destroy(comm);
+  if (rc != 0) return nccl_fail(rc, "ncclCommDestroy");
+  return MOM_OK;
+}
+
+mom_status_t mom_allgather_rows(void *rows, int64_t rows_per_rank, int64_t hidden, mom_dtype_t dt, void *comm,
+                                int rank, int nranks, mom_stream_t stream) {
+  g_err[0] = 0;
+  if (!rows || !comm || rows_per_rank < 1 || hidden < 1 || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(MOM_ERR_INVALID_ARG, "mom_allgather_rows: bad arguments");
+  if (!valid_dtype(dt)) return fail(MOM_ERR_INVALID_ARG, "mom_allgather_rows: bad dtype");
+  if (!aligned16(rows)) return fail(MOM_ERR_INVALID_ARG, "mom_allgather_rows: rows must be 16-byte aligned");
+  Nccl &n = nccl();
+  if (!n.ok) return fail(MOM_ERR_NCCL, "%s", n.why);
+  const size_t count = static_cast<size_t>(rows_per_rank) * static_cast<size_t>(hidden);
+  const size_t w = dtype_bytes(dt);
+  const int nccl_dtype = dt == MOM_BF16 ? 9 /* ncclBfloat16 */ : 7 /* ncclFloat32 */;
+  const void *send = static_cast<const char *>(rows) + static_cast<size_t>(rank) * count * w;  // in-place
+  int rc = n.allgather(send, rows, count, nccl_dtype, comm, static_cast<cudaStream_t>(stream));
+  if (rc != 0) return nccl_fail(rc, "ncclAllGather");
+  return MOM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,270 @@
+// gemv.cu -- HBM-streaming kernels of MOM's last-token path (Alg. 1):
+//   * last_token_mlp: O_last = residual + W_down (Swish(W_gate x) (.) W_up x)
+//       kernel 1 streams W_gate and W_up (2*I*d*w bytes), keeps h in fp32;
+//       kernel 2 streams W_down (d*I*w bytes) with h staged in shared memory.
+//   * lm_head: logits = W_head . rmsnorm(h) and the greedy token
+//       streams W_head (V*d*w bytes) once; per-block packed (value, index) maxima, then a
+//       one-block reduction.  Ties -> lowest index.
+// All are bandwidth-bound: one warp per weight row, 16-byte coalesced vector loads issued
+// in unrolled batches (8 x 16 B in flight per lane), fp32 accumulation, shuffle reductions.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace mom {
+namespace gemv {
+
+constexpr int THREADS = 256;
+constexpr int WARPS = THREADS / 32;
+constexpr int UNROLL = 8;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ uint4 ld_stream(const void *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// dot of 8 bf16 (one 16-B vector) with 8 fp32 from shared memory
+__device__ __forceinline__ float dot8_bf16(const uint4 &w, const float *x) {
+  const __nv_bfloat162 *w2 = reinterpret_cast<const __nv_bfloat162 *>(&w);
+  float s = 0.f;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    float2 f = __bfloat1622float2(w2[e]);
+    s = fmaf(f.x, x[2 * e], s);
+    s = fmaf(f.y, x[2 * e + 1], s);
+  }
+  return s;
+}
+__device__ __forceinline__ float dot4_f32(const uint4 &w, const float *x) {
+  float s = __uint_as_float(w.x) * x[0];
+  s = fmaf(__uint_as_float(w.y), x[1], s);
+  s = fmaf(__uint_as_float(w.z), x[2], s);
+  s = fmaf(__uint_as_float(w.w), x[3], s);
+  return s;
+}
+
+// Warp-level dot product of one weight row (n elements, 16-B aligned) with xs (smem fp32).
+template <bool BF16>
+__device__ __forceinline__ float row_dot(const void *wrow, const float *xs, int n, int lane) {
+  constexpr int EPV = BF16 ? 8 : 4;  // elements per 16-B vector
+  const int nvec = n / EPV;
+  const uint4 *w = reinterpret_cast<const uint4 *>(wrow);
+  float acc = 0.f;
+  int v0 = 0;
+  for (; v0 + 32 * UNROLL <= nvec; v0 += 32 * UNROLL) {
+    uint4 buf[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) buf[u] = ld_stream(w + v0 + u * 32 + lane);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int e = (v0 + u * 32 + lane) * EPV;
+      acc += BF16 ? dot8_bf16(buf[u], xs + e) : dot4_f32(buf[u], xs + e);
+    }
+  }
+  for (int v = v0 + lane; v < nvec; v += 32) {
+    uint4 b = ld_stream(w + v);
+    const int e = v * EPV;
+    acc += BF16 ? dot8_bf16(b, xs + e) : dot4_f32(b, xs + e);
+  }
+  return warp_sum(acc);
+}
+
+template <bool BF16>
+__device__ __forceinline__ float load_elem(const void *p, size_t i) {
+  if (BF16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16 *>(p)[i]);
+  return reinterpret_cast<const float *>(p)[i];
+}
+template <bool BF16>
+__device__ __forceinline__ void store_elem(void *p, size_t i, float v) {
+  if (BF16)
+    reinterpret_cast<__nv_bfloat16 *>(p)[i] = __float2bfloat16_rn(v);
+  else
+    reinterpret_cast<float *>(p)[i] = v;
+}
+
+// h[j] = Swish(sum_k x_k Wg[j,k]) * (sum_k x_k Wu[j,k]), fp32.  Grid-stride over rows j.
+template <bool BF16>
+__global__ void __launch_bounds__(THREADS) gate_up_gemv(const void *__restrict__ x, const void *__restrict__ wg,
+                                                        const void *__restrict__ wu, float *__restrict__ h, int d,
+                                                        int I) {
+  extern __shared__ float xs[];
+  for (int k = threadIdx.x; k < d; k += THREADS) xs[k] = load_elem<BF16>(x, k);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * WARPS + (threadIdx.x >> 5);
+  const size_t pitch = static_cast<size_t>(d) * (BF16 ? 2 : 4);
+  for (int j = w; j < I; j += gridDim.x * WARPS) {
+    const float g = row_dot<BF16>(static_cast<const char *>(wg) + j * pitch, xs, d, lane);
+    const float u = row_dot<BF16>(static_cast<const char *>(wu) + j * pitch, xs, d, lane);
+    if (lane == 0) h[j] = g / (1.0f + __expf(-g)) * u;
+  }
+}
+
+// out[c] = residual[c] + sum_j h_j Wd[c,j].  h (fp32) staged in shared memory.
+template <bool BF16>
+__global__ void __launch_bounds__(THREADS) down_gemv(const float *__restrict__ h, const void *__restrict__ wd,
+                                                     const void *__restrict__ residual, void *__restrict__ out, int d,
+                                                     int I) {
+  extern __shared__ float hs[];
+  for (int j = threadIdx.x; j < I; j += THREADS) hs[j] = h[j];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * WARPS + (threadIdx.x >> 5);
+  const size_t pitch = static_cast<size_t>(I) * (BF16 ? 2 : 4);
+  for (int c = w; c < d; c += gridDim.x * WARPS) {
+    const float o = row_dot<BF16>(static_cast<const char *>(wd) + c * pitch, hs, I, lane);
+    if (lane == 0) {
+      const float r = residual ? load_elem<BF16>(residual, c) : 0.f;
+      store_elem<BF16>(out, c, r + o);
+    }
+  }
+}
+
+// Order-preserving map float -> uint32 (larger float -> larger key), then pack with the
+// complemented index so that the u64 max picks the largest value and, among equal
+// values, the LOWEST index.
+__device__ __forceinline__ unsigned long long pack_key(float v, int idx) {
+  uint32_t b = __float_as_uint(v);
+  b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  return (static_cast<unsigned long long>(b) << 32) | static_cast<uint32_t>(0xFFFFFFFFu - static_cast<uint32_t>(idx));
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long x = __shfl_xor_sync(0xffffffffu, v, o);
+    v = x > v ? x : v;
+  }
+  return v;
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(THREADS) lm_head_gemv(const void *__restrict__ hin, const void *__restrict__ gain,
+                                                        float eps, const void *__restrict__ w,
+                                                        float *__restrict__ logits,
+                                                        unsigned long long *__restrict__ partials, int d, int V) {
+  extern __shared__ float hs[];
+  __shared__ float red[WARPS];
+  __shared__ unsigned long long best_s[WARPS];
+  // prologue: fp32 copy of h and (optionally) the final RMSNorm
+  float ss = 0.f;
+  for (int k = threadIdx.x; k < d; k += THREADS) {
+    const float v = load_elem<BF16>(hin, k);
+    hs[k] = v;
+    ss += v * v;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (gain) {
+    ss = warp_sum(ss);
+    if (lane == 0) red[wid] = ss;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int i = 0; i < WARPS; ++i) tot += red[i];
+    const float inv = rsqrtf(tot / static_cast<float>(d) + eps);
+    for (int k = threadIdx.x; k < d; k += THREADS) hs[k] = hs[k] * inv * load_elem<BF16>(gain, k);
+  }
+  __syncthreads();
+  const int wglob = blockIdx.x * WARPS + wid;
+  const size_t pitch = static_cast<size_t>(d) * (BF16 ? 2 : 4);
+  unsigned long long best = 0ull;
+  for (int v = wglob; v < V; v += gridDim.x * WARPS) {
+    const float s = row_dot<BF16>(static_cast<const char *>(w) + v * pitch, hs, d, lane);
+    if (lane == 0) {
+      if (logits) logits[v] = s;
+      const unsigned long long key = pack_key(s, v);
+      best = key > best ? key : best;
+    }
+  }
+  if (lane == 0) best_s[wid] = best;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long b = lane < WARPS ? best_s[lane] : 0ull;
+    b = warp_max_u64(b);
+    if (lane == 0) partials[blockIdx.x] = b;
+  }
+}
+
+__global__ void argmax_reduce(const unsigned long long *__restrict__ partials, int n, int32_t *__restrict__ out) {
+  __shared__ unsigned long long s[32];
+  unsigned long long b = 0ull;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) b = partials[i] > b ? partials[i] : b;
+  b = warp_max_u64(b);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    b = threadIdx.x < blockDim.x / 32 ? s[threadIdx.x] : 0ull;
+    b = warp_max_u64(b);
+    if (threadIdx.x == 0) out[0] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(b & 0xFFFFFFFFull));
+  }
+}
+
+template <typename K>
+static cudaError_t set_smem(K kfn, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+}
+
+}  // namespace gemv
+
+cudaError_t launch_last_token_mlp(const void *x, const void *residual, const void *wg, const void *wu,
+                                  const void *wd, void *out, float *h_ws, int d, int I, bool is_bf16, int num_sms,
+                                  cudaStream_t stream) {
+  using namespace gemv;
+  const size_t smem1 = static_cast<size_t>(d) * sizeof(float);
+  const size_t smem2 = static_cast<size_t>(I) * sizeof(float);
+  // kernel 1: 2 rows (gate+up) per warp per step; enough warps for several MB in flight
+  int blocks1 = (I + WARPS - 1) / WARPS;
+  if (blocks1 > num_sms * 8) blocks1 = num_sms * 8;
+  int blocks2 = (d + WARPS - 1) / WARPS;
+  if (blocks2 > num_sms * 4) blocks2 = num_sms * 4;
+  cudaError_t e;
+  if (is_bf16) {
+    if ((e = set_smem(gate_up_gemv<true>, smem1)) != cudaSuccess) return e;
+    if ((e = set_smem(down_gemv<true>, smem2)) != cudaSuccess) return e;
+    gate_up_gemv<true><<<blocks1, THREADS, smem1, stream>>>(x, wg, wu, h_ws, d, I);
+    down_gemv<true><<<blocks2, THREADS, smem2, stream>>>(h_ws, wd, residual, out, d, I);
+  } else {
+    if ((e = set_smem(gate_up_gemv<false>, smem1)) != cudaSuccess) return e;
+    if ((e = set_smem(down_gemv<false>, smem2)) != cudaSuccess) return e;
+    gate_up_gemv<false><<<blocks1, THREADS, smem1, stream>>>(x, wg, wu, h_ws, d, I);
+    down_gemv<false><<<blocks2, THREADS, smem2, stream>>>(h_ws, wd, residual, out, d, I);
+  }
+  return cudaGetLastError();
+}
+
+size_t lm_head_partials(int num_sms) { return static_cast<size_t>(num_sms) * 4; }
+
+cudaError_t launch_lm_head(const void *h, const void *gain, float eps, const void *w, float *logits,
+                           int32_t *argmax, unsigned long long *partials, int d, int V, bool is_bf16, int num_sms,
+                           cudaStream_t stream) {
+  using namespace gemv;
+  const size_t smem = static_cast<size_t>(d) * sizeof(float);
+  int blocks = static_cast<int>(lm_head_partials(num_sms));
+  const int need = (V + WARPS - 1) / WARPS;
+  if (blocks > need) blocks = need;
+  cudaError_t e;
+  if (is_bf16) {
+    if ((e = set_smem(lm_head_gemv<true>, smem)) != cudaSuccess) return e;
+    lm_head_gemv<true><<<blocks, THREADS, smem, stream>>>(h, gain, eps, w, logits, partials, d, V);
+  } else {
+    if ((e = set_smem(lm_head_gemv<false>, smem)) != cudaSuccess) return e;
+    lm_head_gemv<false><<<blocks, THREADS, smem, stream>>>(h, gain, eps, w, logits, partials, d, V);
+  }
+  argmax_reduce<<<1, 1024, 0, stream>>>(partials, blocks, argmax);
+  return cudaGetLastError();
+}
+
+}  // namespace mom

@@ -1,0 +1,370 @@
+// mlp_tc.cu -- tcgen05/TMEM/TMA kernels for the bf16 mini-sequence SwiGLU MLP
+// (Alg. 1 P:109-113 of arXiv 2504.12526; MLP = SwiGLU).
+//
+// One persistent, warp-specialised "dual-B" GEMM serves both phases of a mini-sequence:
+//
+//   Phase A  (gate/up + SiLU*mul):  acc[:, 0:128]   = X_i Wg[n0:n0+128]^T
+//                                   acc[:, 128:256] = X_i Wu[n0:n0+128]^T
+//            epilogue  H_i[:, n0:n0+128] = bf16( silu(acc[:, j]) * acc[:, 128+j] )
+//   Phase B  (down + residual):     acc[:, 0:256]   = H_i Wd[n0:n0+256]^T
+//            epilogue  out[:, n0:n0+256] = bf16( residual + acc )
+//
+// so one UMMA with N = 256 computes the gate and up tiles of the same 128 intermediate
+// columns side by side in TMEM, and the [S, I] gate/up tensors never exist (Eq. 1).
+//
+// Roles (256 threads): warp 0 = TMA producer (1 lane), warp 1 = TMEM allocator + MMA issuer
+// (1 lane), warps 4..7 = epilogue (TMEM lane quarter q = warp - 4, one row per thread).
+// Pipelines: smem stages full/empty (TMA <-> MMA), TMEM accumulators full/empty x2
+// (MMA <-> epilogue, 2 x 256 fp32 columns = all 512 TMEM columns).
+//
+// CG = 1: one CTA per tile, UMMA M = 128, the CTA stages both B halves (Wg and Wu rows).
+// CG = 2: a CTA pair (cluster of 2) per tile, UMMA M = 256 (cta_group::2): CTA r stages
+//         A rows [128r, 128r+128) and B half r; the leader CTA issues the MMAs; both CTAs
+//         hold their 128 rows x 256 columns of the accumulator in their own TMEM.
+//
+// Determinism: no split-K, no atomics, the tile shape does not depend on the mini-sequence
+// length, and every accumulator sums K in the same order -> outputs are bitwise identical
+// for every mini-sequence count M (the paper's "identical logits").
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ptx.cuh"
+#include "kernels.h"
+
+namespace mom {
+
+namespace tc {
+
+constexpr uint32_t BM = 128;         // rows per CTA
+constexpr uint32_t BK = 64;          // K per stage (64 bf16 = 128 B = one swizzle span)
+constexpr uint32_t BHALF = 128;      // rows per B half
+constexpr uint32_t UMMA_N = 256;     // both B halves
+constexpr uint32_t UMMA_K = 16;      // fixed for kind::f16
+constexpr uint32_t A_BYTES = BM * BK * 2;        // 16 KB
+constexpr uint32_t BHALF_BYTES = BHALF * BK * 2; // 16 KB
+constexpr uint32_t ACC_COLS = 256;
+constexpr uint32_t NUM_THREADS = 256;
+constexpr uint32_t EPI_WARP0 = 4;
+
+template <int CG>
+struct Cfg {
+  static constexpr uint32_t B_BYTES = (CG == 1 ? 2 : 1) * BHALF_BYTES;  // B bytes staged per CTA
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t STAGES = CG == 1 ? 4 : 6;
+  static constexpr uint32_t TX_BYTES = STAGE_BYTES * CG;  // bytes landing per stage per tile
+  static constexpr uint32_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+};
+
+struct Params {
+  // problem
+  uint32_t rows;         // valid rows of this mini-sequence (C_i)
+  uint32_t n_out;        // output columns (I for phase A, d for phase B)
+  uint32_t k;            // reduction length (d for phase A, I for phase B)
+  uint32_t m_tiles;      // ceil(rows / (BM*CG))
+  uint32_t n_tiles;      // ceil(n_out / tile_n)
+  uint32_t group_m;      // raster: M tiles per group (N iterates inside a group)
+  // epilogue
+  __nv_bfloat16 *out;            // phase A: H_i [rows, I]; phase B: out rows [rows, d]
+  const __nv_bfloat16 *residual; // phase B only, may be null
+  uint32_t ld_out;               // row pitch (elements) of out / residual
+};
+
+__device__ __forceinline__ void tile_coords(uint32_t t, const Params &p, uint32_t &m, uint32_t &n) {
+  const uint32_t per_group = p.group_m * p.n_tiles;
+  const uint32_t g = t / per_group;
+  const uint32_t local = t - g * per_group;
+  const uint32_t m0 = g * p.group_m;
+  uint32_t gm = p.m_tiles - m0;
+  if (gm > p.group_m) gm = p.group_m;
+  m = m0 + local % gm;
+  n = local / gm;
+}
+
+__device__ __forceinline__ float silu_mul(float g, float u) {
+  // Swish(g) * u = g * sigmoid(g) * u, fp32
+  return g / (1.0f + __expf(-g)) * u;
+}
+
+template <int CG, bool PHASE_A>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    dual_b_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b0,
+                       const __grid_constant__ CUtensorMap tm_b1, const Params p) {
+  using C = Cfg<CG>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B alignment for the SWIZZLE_128B atoms
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *smem_a = smem;                                   // STAGES x A_BYTES
+  uint8_t *smem_b = smem + C::STAGES * A_BYTES;             // STAGES x B_BYTES
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t *full = bars;                       // [STAGES]
+  uint64_t *empty = bars + C::STAGES;          // [STAGES]
+  uint64_t *tfull = bars + 2 * C::STAGES;      // [2]
+  uint64_t *tempty = bars + 2 * C::STAGES + 2; // [2]
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * C::STAGES + 4);
+
+  const uint32_t warp = ptx::warp_id();
+  const uint32_t lane = ptx::lane_id();
+  const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0;
+  const bool leader = (rank == 0);
+  const uint32_t cluster_id = blockIdx.x / CG;
+  const uint32_t num_clusters = gridDim.x / CG;
+  const uint32_t num_tiles = p.m_tiles * p.n_tiles;
+  const uint32_t num_kb = (p.k + BK - 1) / BK;
+  constexpr uint32_t TILE_N = PHASE_A ? BHALF : UMMA_N;  // output columns per tile
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tm_a);
+    ptx::prefetch_tmap(&tm_b0);
+    ptx::prefetch_tmap(&tm_b1);
+    for (uint32_t s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (uint32_t a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 4 * CG);  // one arrival per epilogue warp of every CTA
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc<CG>(tmem_holder, 2 * ACC_COLS);
+  }
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      const uint64_t pol_a = PHASE_A ? ptx::policy_evict_last() : ptx::policy_evict_normal();
+      const uint64_t pol_b = PHASE_A ? ptx::policy_evict_normal() : ptx::policy_evict_last();
+      const uint32_t full_leader0 = (CG == 2) ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : ptx::smem_u32(&full[0]);
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t t = cluster_id; t < num_tiles; t += num_clusters) {
+        uint32_t mt, nt;
+        tile_coords(t, p, mt, nt);
+        const int32_t a_row = static_cast<int32_t>(mt * BM * CG + rank * BM);
+        const int32_t b_row0 = static_cast<int32_t>(nt * TILE_N);
+        for (uint32_t kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          const int32_t kc = static_cast<int32_t>(kb * BK);
+          const uint32_t sa = ptx::smem_u32(smem_a + stage * A_BYTES);
+          const uint32_t sb = ptx::smem_u32(smem_b + stage * C::B_BYTES);
+          const uint32_t fbar = full_leader0 + stage * 8;
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], C::TX_BYTES);
+          if constexpr (CG == 1) {
+            ptx::tma_load_2d(&tm_a, sa, fbar, kc, a_row, pol_a);
+            ptx::tma_load_2d(&tm_b0, sb, fbar, kc, b_row0, pol_b);
+            ptx::tma_load_2d(&tm_b1, sb + BHALF_BYTES, fbar, kc, b_row0 + (PHASE_A ? 0 : (int32_t)BHALF), pol_b);
+          } else {
+            ptx::tma_load_2d_cg2(&tm_a, sa, fbar, kc, a_row, pol_a);
+            if (rank == 0)
+              ptx::tma_load_2d_cg2(&tm_b0, sb, fbar, kc, b_row0, pol_b);
+            else
+              ptx::tma_load_2d_cg2(&tm_b1, sb, fbar, kc, b_row0 + (PHASE_A ? 0 : (int32_t)BHALF), pol_b);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+      // Tail: wait until the MMA released every stage, so no tcgen05.commit arrival is still
+      // in flight towards this CTA's shared memory when it exits.
+      for (uint32_t i = 0; i < C::STAGES; ++i) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer (leader CTA, one thread) =======================
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM * CG, UMMA_N);
+      uint32_t stage = 0, phase = 0;
+      uint32_t acc = 0, acc_phase = 0;
+      for (uint32_t t = cluster_id; t < num_tiles; t += num_clusters) {
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * ACC_COLS;
+        for (uint32_t kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint64_t adesc = ptx::sw128_kmajor_desc(ptx::smem_u32(smem_a + stage * A_BYTES));
+          const uint64_t bdesc = ptx::sw128_kmajor_desc(ptx::smem_u32(smem_b + stage * C::B_BYTES));
+#pragma unroll
+          for (uint32_t k = 0; k < BK / UMMA_K; ++k) {
+            // advance 16 bf16 = 32 B along K inside the 128-B swizzle span (>>4 -> +2)
+            ptx::mma_bf16<CG>(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          ptx::mma_commit<CG>(&empty[stage], 0x3);  // frees the smem stage (both CTAs for CG=2)
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        ptx::mma_commit<CG>(&tfull[acc], 0x3);      // accumulator ready for the epilogue(s)
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ======================= epilogue: TMEM -> registers -> global =======================
+    const uint32_t q = warp - EPI_WARP0;  // TMEM lane quarter
+    const uint32_t row_in_tile = q * 32 + lane;
+    uint32_t acc = 0, acc_phase = 0;
+    const uint32_t tempty_leader = (CG == 2) ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0;
+    for (uint32_t t = cluster_id; t < num_tiles; t += num_clusters) {
+      uint32_t mt, nt;
+      tile_coords(t, p, mt, nt);
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const uint32_t row = mt * BM * CG + rank * BM + row_in_tile;
+      const bool row_ok = row < p.rows;
+      const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * ACC_COLS;
+      const uint32_t col0 = nt * TILE_N;
+      if constexpr (PHASE_A) {
+        __nv_bfloat16 *orow = p.out + static_cast<size_t>(row) * p.ld_out + col0;
+#pragma unroll 1
+        for (uint32_t c = 0; c < BHALF / 32; ++c) {
+          uint32_t g[32], u[32];
+          ptx::tmem_ld_32x32b_x32(taddr + c * 32, g);
+          ptx::tmem_ld_32x32b_x32(taddr + BHALF + c * 32, u);
+          ptx::tmem_ld_wait();
+          uint32_t packed[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float h0 = silu_mul(__uint_as_float(g[2 * i]), __uint_as_float(u[2 * i]));
+            float h1 = silu_mul(__uint_as_float(g[2 * i + 1]), __uint_as_float(u[2 * i + 1]));
+            packed[i] = ptx::pack_bf16x2(h0, h1);
+          }
+          if (row_ok) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              if (col0 + c * 32 + v * 8 < p.n_out) {
+                uint4 w = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+                *reinterpret_cast<uint4 *>(orow + c * 32 + v * 8) = w;
+              }
+            }
+          }
+        }
+      } else {
+        __nv_bfloat16 *orow = p.out + static_cast<size_t>(row) * p.ld_out + col0;
+        const __nv_bfloat16 *rrow = p.residual ? p.residual + static_cast<size_t>(row) * p.ld_out + col0 : nullptr;
+#pragma unroll 1
+        for (uint32_t c = 0; c < UMMA_N / 32; ++c) {
+          uint32_t a[32];
+          ptx::tmem_ld_32x32b_x32(taddr + c * 32, a);
+          ptx::tmem_ld_wait();
+          if (row_ok) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const uint32_t col = col0 + c * 32 + v * 8;
+              if (col < p.n_out) {
+                float r[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                if (rrow) {
+                  uint4 rv = *reinterpret_cast<const uint4 *>(rrow + c * 32 + v * 8);
+                  const __nv_bfloat162 *r2 = reinterpret_cast<const __nv_bfloat162 *>(&rv);
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    float2 f = __bfloat1622float2(r2[e]);
+                    r[2 * e] = f.x;
+                    r[2 * e + 1] = f.y;
+                  }
+                }
+                uint4 w;
+                w.x = ptx::pack_bf16x2(r[0] + __uint_as_float(a[8 * v + 0]), r[1] + __uint_as_float(a[8 * v + 1]));
+                w.y = ptx::pack_bf16x2(r[2] + __uint_as_float(a[8 * v + 2]), r[3] + __uint_as_float(a[8 * v + 3]));
+                w.z = ptx::pack_bf16x2(r[4] + __uint_as_float(a[8 * v + 4]), r[5] + __uint_as_float(a[8 * v + 5]));
+                w.w = ptx::pack_bf16x2(r[6] + __uint_as_float(a[8 * v + 6]), r[7] + __uint_as_float(a[8 * v + 7]));
+                *reinterpret_cast<uint4 *>(orow + c * 32 + v * 8) = w;
+              }
+            }
+          }
+        }
+      }
+      // release the accumulator to the MMA issuer
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          ptx::mbar_arrive_cluster(tempty_leader + acc * 8);
+        else
+          ptx::mbar_arrive(&tempty[acc]);
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<CG>(tmem_base, 2 * ACC_COLS);
+  }
+}
+
+template <int CG, bool PHASE_A>
+static cudaError_t launch(const CUtensorMap &tm_a, const CUtensorMap &tm_b0, const CUtensorMap &tm_b1,
+                          const Params &p, int num_sms, cudaStream_t stream) {
+  using C = Cfg<CG>;
+  auto kfn = dual_b_gemm_kernel<CG, PHASE_A>;
+  static thread_local int configured_device = -1;  // attribute is per device; cheap to re-set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (configured_device != dev) {
+    e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured_device = dev;
+  }
+  const uint32_t num_tiles = p.m_tiles * p.n_tiles;
+  uint32_t clusters = static_cast<uint32_t>(num_sms) / CG;
+  if (clusters > num_tiles) clusters = num_tiles;
+  if (clusters == 0) clusters = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(clusters * CG, 1, 1);
+  cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kfn, tm_a, tm_b0, tm_b1, p);
+}
+
+}  // namespace tc
+
+cudaError_t launch_phase_a_tc(const TcPhaseArgs &a, cudaStream_t stream) {
+  tc::Params p{};
+  p.rows = a.rows;
+  p.n_out = a.n_out;
+  p.k = a.k;
+  p.m_tiles = (a.rows + tc::BM * a.cta_group - 1) / (tc::BM * a.cta_group);
+  p.n_tiles = (a.n_out + tc::BHALF - 1) / tc::BHALF;
+  p.group_m = a.group_m ? a.group_m : p.m_tiles;
+  if (p.group_m > p.m_tiles) p.group_m = p.m_tiles;
+  p.out = a.out;
+  p.residual = nullptr;
+  p.ld_out = a.ld_out;
+  if (a.cta_group == 2) return tc::launch<2, true>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
+  return tc::launch<1, true>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
+}
+
+cudaError_t launch_phase_b_tc(const TcPhaseArgs &a, cudaStream_t stream) {
+  tc::Params p{};
+  p.rows = a.rows;
+  p.n_out = a.n_out;
+  p.k = a.k;
+  p.m_tiles = (a.rows + tc::BM * a.cta_group - 1) / (tc::BM * a.cta_group);
+  p.n_tiles = (a.n_out + tc::UMMA_N - 1) / tc::UMMA_N;
+  p.group_m = a.group_m ? a.group_m : 8;
+  if (p.group_m > p.m_tiles) p.group_m = p.m_tiles;
+  p.out = a.out;
+  p.residual = a.residual;
+  p.ld_out = a.ld_out;
+  if (a.cta_group == 2) return tc::launch<2, false>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
+  return tc::launch<1, false>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
+}
+
+}  // namespace mom

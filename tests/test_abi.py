@@ -1,0 +1,103 @@
+"""CPU-side checks of the C ABI (no kernel launches): libmom.so loads, exports every symbol
+include/mom.h declares, the host-only planner and workspace queries follow the paper
+(Alg. 1, Eq. 3), and invalid arguments are rejected before any CUDA call."""
+from __future__ import annotations
+
+import ctypes
+import json
+import math
+import os
+import re
+import subprocess
+
+import pytest
+
+import oracle
+from paper_2504_12526_b200 import _mom
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = json.load(open(os.path.join(ROOT, "tests", "golden", "spec_worked_examples.json")))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2504_12526_b200 import build
+    build.build()
+    return _mom.lib()
+
+
+def declared_symbols():
+    hdr = open(os.path.join(ROOT, "include", "mom.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    return sorted(set(re.findall(r"\b(mom_[a-z0-9_]+)\s*\(", hdr)))
+
+
+def test_every_declared_symbol_is_exported(lib):
+    syms = declared_symbols()
+    assert len(syms) >= 15
+    out = subprocess.run(["nm", "-D", "--defined-only", _mom.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (mom_[a-z0-9_]+)", out))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    # and the binding's signature table covers exactly the declared ABI
+    assert sorted(_mom.SIGNATURES) == syms
+
+
+def test_library_is_sm100a(lib):
+    out = subprocess.run(["cuobjdump", "--list-elf", _mom.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", _mom.LIB_PATH], capture_output=True, text=True).stdout
+    # tcgen05.mma (UTCHMMA, incl. the 2-CTA form), TMA loads, TMEM loads are in the binary
+    assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
+
+
+@pytest.mark.parametrize("S,C", [(8, 3), (100, 250), (144000, 8192), (155000, 8192), (1, 1), (1024, 256)])
+def test_plan_matches_oracle(lib, S, C):
+    assert _mom.plan_minseq(S, C) == oracle.plan(S, C)
+
+
+def test_plan_rejects_bad_sizes(lib):
+    assert lib.mom_plan_minseq(0, 4, None, None, 0) == -1
+    assert lib.mom_plan_minseq(5, 0, None, None, 0) == -1
+
+
+def test_workspace_is_one_minisequence(lib):
+    """Eq. 3: the transient is S*I*w / M: with SPEC's numbers 131072 B."""
+    g = GOLD["eq3_bytes"]
+    C = math.ceil(g["S"] / g["M"])
+    ws = lib.mom_mlp_minseq_workspace_bytes(g["S"], 64, g["I"], C, _mom.MOM_F32)
+    assert ws == g["expect"]
+    g1 = GOLD["eq1_bytes"]  # C >= S: the unchunked Eq. 1 S*I*w
+    assert lib.mom_mlp_minseq_workspace_bytes(g1["S"], 64, g1["I"], 10**9, _mom.MOM_F32) == g1["expect"]
+    # config 2 (Llama MLP, S=65536, M=8, bf16): 8192 * 14336 * 2 bytes = 235 MB vs 1.88 GB
+    assert lib.mom_mlp_minseq_workspace_bytes(65536, 4096, 14336, 8192, _mom.MOM_BF16) == 8192 * 14336 * 2
+    assert lib.mom_mlp_minseq_workspace_bytes(0, 4096, 14336, 8192, _mom.MOM_BF16) == 0
+
+
+def _call_fwd(lib, **over):
+    args = dict(x=16, residual=None, wg=32, wu=48, wd=64, out=80, S=4, d=8, I=16, C=2, dt=_mom.MOM_BF16,
+                ws=96, ws_bytes=1 << 20, stream=None)
+    args.update(over)
+    return lib.mom_mlp_minseq_fwd(args["x"], args["residual"], args["wg"], args["wu"], args["wd"], args["out"],
+                                  args["S"], args["d"], args["I"], args["C"], args["dt"], args["ws"],
+                                  args["ws_bytes"], args["stream"])
+
+
+def test_invalid_arguments_rejected_before_launch(lib):
+    E = _mom.MOM_ERR_INVALID_ARG
+    assert _call_fwd(lib, x=None) == E
+    assert _call_fwd(lib, S=0) == E
+    assert _call_fwd(lib, C=0) == E
+    assert _call_fwd(lib, d=6) == E               # 12-byte row pitch: not TMA-legal
+    assert _call_fwd(lib, wg=40) == E             # misaligned
+    assert _call_fwd(lib, dt=7) == E
+    assert "16" in lib.mom_last_error().decode() or "dtype" in lib.mom_last_error().decode()
+    # out partially overlapping x: x=16 spans 4*8*2 = 64 bytes
+    assert _call_fwd(lib, out=32, wg=128) == E
+    assert _call_fwd(lib, ws_bytes=10) == _mom.MOM_ERR_WORKSPACE
+    assert lib.mom_lm_head_last(None, None, 0.0, 16, None, 32, 8, 10, 0, 48, 1 << 16, None) == E
+    assert lib.mom_mlp_last_token(16, None, 32, 48, 64, 80, 8, 0, 0, 96, 1 << 16, None) == E
+    assert lib.mom_kv_offload(None, 16, 10, None, None, None) == E
+    assert lib.mom_kv_reload(16, None, 10, None, None) == E
+    assert lib.mom_allgather_rows(16, 4, 8, 0, None, 0, 2, None) == E
+    assert lib.mom_nccl_comm_init(None, 2, None, 0) == E

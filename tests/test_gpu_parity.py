@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs (synth/), plus the exact GPU-only invariants.  All tests need a B200: -m gpu.
+
+Bars (BASELINE.json north_star):
+  bf16 MLP: normwise max relative error <= 2e-2 per tensor and per row;
+  fp32 MLP: <= 1e-4;  argmax: bit-exact (decided on the same fp32 logits), tie-guarded
+  against the float64 oracle;  bit-identity across mini-sequence counts; KV round trip exact.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2504_12526_b200 import _mom
+from tests.parity import TOL_BF16, TOL_F32, argmax_matches, check_close
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _cta_group_env():
+    old = os.environ.get("MOM_CTA_GROUP")
+    yield
+    if old is None:
+        os.environ.pop("MOM_CTA_GROUP", None)
+    else:
+        os.environ["MOM_CTA_GROUP"] = old
+
+
+def _mlp_inputs(S, d, I, dtype, device, layer=0, residual=True):
+    wg, wu, wd = synth.mlp_weights(d, I, layer, "cpu", dtype)
+    x = synth.hidden(S, d, "cpu", dtype)
+    res = synth.hidden(S, d, "cpu", dtype, seed=synth.SEED_X + 1) if residual else None
+    dev = lambda t: None if t is None else t.to(device)  # noqa: E731
+    return (x, res, wg, wu, wd), tuple(dev(t) for t in (x, res, wg, wu, wd))
+
+
+def _run_fwd(gx, gres, gwg, gwu, gwd, C, out=None):
+    out = torch.empty_like(gx) if out is None else out
+    _mom.mlp_minseq_fwd(gx, gres, gwg, gwu, gwd, out, C)
+    torch.cuda.synchronize()
+    return out
+
+
+# ------------------------------------------------------------------ config 1 (fp32 SIMT)
+def test_cfg1_f32_full_tensor(cuda_device):
+    w = synth.CONFIGS[0]
+    (x, res, wg, wu, wd), g = _mlp_inputs(w.S, w.hidden, w.intermediate, torch.float32, cuda_device)
+    out = _run_fwd(*g, C=w.C)
+    ref = oracle.mlp_minseq(x, res, wg, wu, wd, C=w.C)
+    check_close(out, ref, TOL_F32, "cfg1 f32 with residual")
+    out0 = _run_fwd(g[0], None, *g[2:], C=w.C)  # Alg. 1's O_i = MLP(A_i), no residual
+    ref0 = oracle.mlp_minseq(x, None, wg, wu, wd, C=w.C)
+    check_close(out0, ref0, TOL_F32, "cfg1 f32 no residual")
+    for C in (1, 7, 1000, w.S, w.S + 5):  # bit-identity across M on the GPU
+        assert torch.equal(_run_fwd(*g, C=C), out), C
+
+
+# ------------------------------------------------------------------ bf16 tcgen05, small + ragged
+@pytest.mark.parametrize("cta_group", ["1", "2"])
+@pytest.mark.parametrize("S,d,I,C", [(1024, 256, 688, 256), (1000, 512, 1024, 300), (77, 256, 384, 64),
+                                     (300, 384, 640, 300)])
+def test_bf16_tcgen05_vs_oracle(cuda_device, cta_group, S, d, I, C):
+    os.environ["MOM_CTA_GROUP"] = cta_group
+    (x, res, wg, wu, wd), g = _mlp_inputs(S, d, I, torch.bfloat16, cuda_device)
+    out = _run_fwd(*g, C=C)
+    ref = oracle.mlp_minseq(x, res, wg, wu, wd, C=C)
+    check_close(out, ref, TOL_BF16, f"bf16 S={S} d={d} I={I} C={C} cg={cta_group}")
+    out0 = _run_fwd(g[0], None, *g[2:], C=C)
+    ref0 = oracle.mlp_minseq(x, None, wg, wu, wd, C=C)
+    check_close(out0, ref0, TOL_BF16, "bf16 no residual")
+
+
+@pytest.mark.parametrize("cta_group", ["1", "2"])
+def test_bf16_bit_identical_across_M(cuda_device, cta_group):
+    """P:286 identical logits <- P:109-113 row partition: GPU output bitwise equal for every C."""
+    os.environ["MOM_CTA_GROUP"] = cta_group
+    S, d, I = 1000, 256, 688
+    _, g = _mlp_inputs(S, d, I, torch.bfloat16, cuda_device)
+    ref = _run_fwd(*g, C=S)
+    for C in (1, 100, 128, 129, 256, 333, 999, S + 7):
+        assert torch.equal(_run_fwd(*g, C=C), ref), C
+
+
+def test_bf16_cta_groups_agree(cuda_device):
+    S, d, I = 700, 512, 1536
+    _, g = _mlp_inputs(S, d, I, torch.bfloat16, cuda_device)
+    os.environ["MOM_CTA_GROUP"] = "1"
+    a = _run_fwd(*g, C=256)
+    os.environ["MOM_CTA_GROUP"] = "2"
+    b = _run_fwd(*g, C=256)
+    assert torch.equal(a, b)
+
+
+def test_bf16_in_place(cuda_device):
+    """out may alias residual and x (the layer loop's x_{l+1} = x_l + MLP(x_l))."""
+    S, d, I = 640, 256, 512
+    (x, _, wg, wu, wd), g = _mlp_inputs(S, d, I, torch.bfloat16, cuda_device, residual=False)
+    gx = g[0].clone()
+    ref = _run_fwd(g[0], g[0], *g[2:], C=200)
+    _mom.mlp_minseq_fwd(gx, gx, g[2], g[3], g[4], gx, 200)
+    torch.cuda.synchronize()
+    assert torch.equal(gx, ref)
+
+
+# ------------------------------------------------------------------ config 2 at full size
+def test_cfg2_llama_full_size_sampled_rows(cuda_device):
+    """BASELINE config 2 (d=4096, I=14336, S=65536, M=8) in the bench's launch configuration;
+    the oracle checks sampled rows (random + 0, S-1 and both sides of every boundary)."""
+    w = synth.CONFIGS[1]
+    wg, wu, wd = synth.mlp_weights(w.hidden, w.intermediate, 0, cuda_device, torch.bfloat16)
+    x = synth.hidden(w.S, w.hidden, cuda_device, torch.bfloat16)
+    out = torch.empty_like(x)
+    _mom.mlp_minseq_fwd(x, x, wg, wu, wd, out, w.C)
+    torch.cuda.synchronize()
+    rows = synth.sample_rows(w.S, w.C, n_random=96)
+    xs = x.cpu()
+    ref = oracle.mlp_rows(xs, xs, wg.cpu(), wu.cpu(), wd.cpu(), rows)
+    check_close(out[rows].cpu(), ref, TOL_BF16, "cfg2 sampled rows")
+
+
+# ------------------------------------------------------------------ last token + LM head
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_last_token_mlp_and_lm_head(cuda_device, cfg):
+    w = synth.CONFIGS[cfg]
+    dt = synth.torch_dtype(w.dtype)
+    d, I, V = w.hidden, w.intermediate, w.vocab
+    wg, wu, wd = synth.mlp_weights(d, I, 0, "cpu", dt)
+    wh = synth.head_weight(V, d, "cpu", dt)
+    gain = synth.norm_gain(d, "cpu", dt)
+    x = synth.hidden(4, d, "cpu", dt)  # rows of the final layer's input; the last one is used
+    res = synth.hidden(4, d, "cpu", dt, seed=synth.SEED_X + 1)
+    G = lambda t: t.to(cuda_device)  # noqa: E731
+    y = torch.empty(d, dtype=dt, device=cuda_device)
+    _mom.mlp_last_token(G(x)[3], G(res)[3], G(wg), G(wu), G(wd), y)
+    logits = torch.empty(V, dtype=torch.float32, device=cuda_device)
+    am = torch.empty(1, dtype=torch.int32, device=cuda_device)
+    _mom.lm_head_last(y, G(gain), w.eps, G(wh), logits, am)
+    torch.cuda.synchronize()
+    tol = TOL_F32 if w.dtype == "f32" else TOL_BF16
+    y_ref = oracle.mlp_rows(x, res, wg, wu, wd, [3])[0]
+    check_close(y.cpu(), y_ref, tol, "last-token MLP")
+    # LM head checked on the GPU's own hidden vector (same input to both sides)
+    yn = oracle.rmsnorm(y.cpu().double().numpy(), gain, w.eps)
+    ref_logits = oracle.lm_head(yn, wh)[0]
+    check_close(logits.cpu(), ref_logits, 1e-4, "lm head logits")
+    # argmax: bit-exact on the kernel's fp32 logits; tie-guarded against the float64 oracle
+    assert int(am.item()) == oracle.argmax_f32(logits.cpu().numpy())
+    argmax_matches(int(am.item()), ref_logits)
+    # no-norm variant and logits=NULL variant give the same argmax as their logits
+    _mom.lm_head_last(y, None, 0.0, G(wh), logits, am)
+    am2 = torch.empty(1, dtype=torch.int32, device=cuda_device)
+    _mom.lm_head_last(y, None, 0.0, G(wh), None, am2)
+    torch.cuda.synchronize()
+    assert int(am.item()) == int(am2.item()) == oracle.argmax_f32(logits.cpu().numpy())
+    check_close(logits.cpu(), oracle.lm_head(y.cpu().double().numpy(), wh)[0], 1e-4, "lm head no norm")
+
+
+def test_argmax_ties_lowest_index(cuda_device):
+    """S:333 tie at 2 and 5 -> 2, through the real kernel: identity head, h with equal maxima."""
+    d, V = 64, 96
+    wh = torch.zeros(V, d, dtype=torch.bfloat16)
+    for i in range(d):
+        wh[i, i] = 1.0
+    h = torch.zeros(d, dtype=torch.bfloat16)
+    h[2] = h[5] = h[40] = 3.0
+    logits = torch.empty(V, dtype=torch.float32, device=cuda_device)
+    am = torch.empty(1, dtype=torch.int32, device=cuda_device)
+    _mom.lm_head_last(h.to(cuda_device), None, 0.0, wh.to(cuda_device), logits, am)
+    torch.cuda.synchronize()
+    assert int(am.item()) == 2
+    h[70 % d] = -1.0
+    h[:] = -2.0
+    h[63] = -1.5  # all negative: max at 63
+    _mom.lm_head_last(h.to(cuda_device), None, 0.0, wh.to(cuda_device), logits, am)
+    torch.cuda.synchronize()
+    assert int(am.item()) == 63
+
+
+def test_last_token_matches_full_sequence_last_row(cuda_device):
+    """Alg. 1 final branch vs the standard path: GEMV last-token MLP == last row of the
+    mini-sequence MLP within the bf16 bar (both compared to the same oracle row)."""
+    S, d, I = 300, 512, 1024
+    (x, res, wg, wu, wd), g = _mlp_inputs(S, d, I, torch.bfloat16, cuda_device)
+    full = _run_fwd(*g, C=128)
+    y = torch.empty(d, dtype=torch.bfloat16, device=cuda_device)
+    _mom.mlp_last_token(g[0][S - 1], g[1][S - 1], g[2], g[3], g[4], y)
+    torch.cuda.synchronize()
+    ref = oracle.mlp_rows(x, res, wg, wu, wd, [S - 1])[0]
+    check_close(y.cpu(), ref, TOL_BF16, "last token")
+    check_close(full[S - 1].cpu(), ref, TOL_BF16, "full last row")
+
+
+# ------------------------------------------------------------------ KV offload / reload
+def test_kv_offload_reload_roundtrip(cuda_device):
+    """Alg. 1 P:99 / P:106: bytewise round trip; ledger D2H = H2D = 2*S*d_kv*L*w (Eq. 2)."""
+    S, d_kv, L = 4096, 1024, 3
+    kv = [synth.kv_standin(S, d_kv, l, cuda_device) for l in range(L)]
+    host = [torch.empty_like(k, device="cpu").pin_memory() for k in kv]
+    back = [torch.empty_like(k) for k in kv]
+    prod = torch.cuda.current_stream()
+    cp = torch.cuda.Stream()
+    d2h = h2d = 0
+    for l in range(L):
+        done = torch.cuda.Event()
+        _mom.kv_offload(kv[l], host[l], prod, cp, done)
+        d2h += kv[l].numel() * kv[l].element_size()
+    cp.synchronize()
+    for l in range(L):
+        _mom.kv_reload(host[l], back[l], cp)
+        h2d += kv[l].numel() * kv[l].element_size()
+    cp.synchronize()
+    for l in range(L):
+        assert torch.equal(host[l], kv[l].cpu())
+        assert torch.equal(back[l], kv[l])
+    assert d2h == h2d == 2 * S * d_kv * L * 2
+
+
+def test_kv_offload_rejects_pageable_host(cuda_device):
+    kv = torch.zeros(1024, dtype=torch.bfloat16, device=cuda_device)
+    host = torch.empty(1024, dtype=torch.bfloat16)  # not pinned
+    with pytest.raises(_mom.MomError) as ei:
+        _mom.kv_offload(kv, host)
+    assert ei.value.status == _mom.MOM_ERR_INVALID_ARG
+
+
+def test_workspace_too_small_is_reported(cuda_device):
+    S, d, I = 256, 256, 512
+    _, g = _mlp_inputs(S, d, I, torch.bfloat16, cuda_device)
+    ws = torch.empty(1024, dtype=torch.uint8, device=cuda_device)
+    with pytest.raises(_mom.MomError) as ei:
+        _mom.mlp_minseq_fwd(*g, torch.empty_like(g[0]), 128, workspace=ws)
+    assert ei.value.status == _mom.MOM_ERR_WORKSPACE
