@@ -229,7 +229,7 @@ def cpu_baseline(wl, target_s: float = 12.0):
     t0 = time.perf_counter()
     oracle.mlp_rows(x, x, wg, wu, wd, rows, nthreads=threads)
     t1 = time.perf_counter() - t0
-    reps = max(1, min(8, int(target_s / max(t1, 1e-3))))
+    reps = max(1, min(256, int(target_s / max(t1, 1e-3))))
     rows2 = synth.sample_rows(wl.S, wl.C, n_random=threads * reps, seed=synth.SEED_ROWS + 1)[:threads * reps]
     t0 = time.perf_counter()
     oracle.mlp_rows(x, x, wg, wu, wd, rows2, nthreads=threads)

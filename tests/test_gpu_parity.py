@@ -174,12 +174,15 @@ def test_argmax_ties_lowest_index(cuda_device):
     _mom.lm_head_last(h.to(cuda_device), None, 0.0, wh.to(cuda_device), logits, am)
     torch.cuda.synchronize()
     assert int(am.item()) == 2
-    h[70 % d] = -1.0
     h[:] = -2.0
-    h[63] = -1.5  # all negative: max at 63
+    h[63] = -1.5  # logits -2 / -1.5 on the identity rows 0..63, exactly 0 on the zero rows 64..95
     _mom.lm_head_last(h.to(cuda_device), None, 0.0, wh.to(cuda_device), logits, am)
     torch.cuda.synchronize()
-    assert int(am.item()) == 63
+    assert int(am.item()) == 64  # a 32-way tie at 0.0 -> the lowest index
+    wh[95, 0] = -1.0  # row 95: logit +2.0, the unique max
+    _mom.lm_head_last(h.to(cuda_device), None, 0.0, wh.to(cuda_device), logits, am)
+    torch.cuda.synchronize()
+    assert int(am.item()) == 95
 
 
 def test_last_token_matches_full_sequence_last_row(cuda_device):
