@@ -1,0 +1,108 @@
+"""GPU tests of the layer stack (with a6-a10 around it): BASELINE configs 3 and 4 at
+full size.  Parity is per layer and teacher-forced (R12): the oracle receives the GPU's bf16
+input rows of layer l and must reproduce the GPU's output rows of layer l within the bf16 bar; the final
+layer's last-token MLP, the LM head and the argmax are checked on the GPU's own inputs; offloaded K/V
+must match the stand-in bytewise on sampled rows, and the reload must match the host copy."""
+from __future__ import annotations
+
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2504_12526_b200 import _mom
+from paper_2504_12526_b200.stack import PrefillStack
+from tests.parity import TOL_BF16, argmax_matches, check_close
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_stack(cuda_device, d, I, V, L, S, C, d_kv, eps, check_layers, n_rows, offload=True):
+    bf = torch.bfloat16
+    weights = [synth.mlp_weights(d, I, l, cuda_device, bf) for l in range(L)]
+    wh = synth.head_weight(V, d, cuda_device, bf)
+    gain = synth.norm_gain(d, cuda_device, bf)
+    x = synth.hidden(S, d, cuda_device, bf)
+    base = synth.kv_standin(S, d_kv, 0, cuda_device, bf)
+
+    def kv_fill(l, slot):  # attention stand-in: base K/V with the layer id stamped in column 0
+        slot.copy_(base)
+        slot.view(torch.int16)[:, 0] = l
+
+    rows = synth.sample_rows(S, C, n_random=n_rows)
+    snaps = {}
+    want = set(check_layers) | {l + 1 for l in check_layers} | {L - 1}
+
+    def on_layer(l, xx):
+        if l in want:
+            snaps[l] = xx[rows].cpu()
+            if l == L - 1:
+                snaps["last"] = xx[S - 1].cpu()
+
+    stack = PrefillStack(weights, wh, gain, eps, S, C, (S, 2 * d_kv), cuda_device, offload=offload)
+    res = stack.run(x, kv_fill if offload else None, on_layer=on_layer)
+    torch.cuda.synchronize()
+    errs = {}
+    for l in check_layers:
+        wg, wu, wd = (t.cpu() for t in weights[l])
+        inp = snaps[l]
+        ref = oracle.mlp_rows(inp, inp, wg, wu, wd, list(range(len(rows))))
+        errs[l] = check_close(snaps[l + 1], ref, TOL_BF16, f"layer {l} (teacher-forced)")
+    # final layer, last token only (Alg. 1)
+    wg, wu, wd = (t.cpu() for t in weights[L - 1])
+    xl = snaps["last"][None]
+    check_close(res.y_last.cpu(), oracle.mlp_rows(xl, xl, wg, wu, wd, [0])[0], TOL_BF16, "last-token MLP")
+    yn = oracle.rmsnorm(res.y_last.cpu().double().numpy(), gain.cpu(), eps)
+    ref_logits = oracle.lm_head(yn, wh.cpu())[0]
+    check_close(res.logits.cpu(), ref_logits, 1e-4, "LM head")
+    am = int(res.argmax.item())
+    assert am == oracle.argmax_f32(res.logits.cpu().numpy())
+    argmax_matches(am, ref_logits)
+    if offload:
+        kv_rows = synth.sample_rows(S, C, n_random=max(8, S // 100))
+        base_c = base.cpu()[kv_rows]
+        for l in range(L):
+            h = res.kv_host[l][kv_rows]
+            assert torch.equal(h[:, 1:], base_c[:, 1:]), l
+            assert bool((h.view(torch.int16)[:, 0] == l).all()), l
+            assert torch.equal(res.kv_dev[l][kv_rows].cpu(), h), l
+    return errs
+
+
+def test_stack_small(cuda_device):
+    errs = _run_stack(cuda_device, d=256, I=512, V=1000, L=5, S=700, C=256, d_kv=64, eps=1e-5,
+                      check_layers=[0, 1, 2, 3], n_rows=64)
+    assert len(errs) == 4
+
+
+def test_stack_cfg3_qwen_full_size(cuda_device):
+    """BASELINE config 3: Qwen2.5-7B MLP stack, 28 layers (27 mini-sequence + last token), S = 131072,
+    C = 8192 (M = 16), LM head V = 152064, per-layer KV [S, 2*512] offloaded and reloaded."""
+    w = synth.CONFIGS[2]
+    _run_stack(cuda_device, w.hidden, w.intermediate, w.vocab, w.layers, w.S, w.C, w.d_kv, w.eps,
+               check_layers=[0, w.layers // 2, w.layers - 2], n_rows=24)
+
+
+def test_stack_cfg4_mistral_full_size(cuda_device):
+    """BASELINE config 4: Mistral-NeMo-12B, 40 layers, S = 155000 (M = 19, tail 7544 rows), per-layer
+    KV [S, 2*1024] bf16 (635 MB) offloaded to pinned host (25.4 GB) and reloaded."""
+    import psutil
+    w = synth.CONFIGS[3]
+    need = w.layers * w.S * 2 * w.d_kv * 2
+    if psutil.virtual_memory().available < 2 * need:
+        pytest.skip(f"host has {psutil.virtual_memory().available / 1e9:.0f} GB free, needs {2 * need / 1e9:.0f} GB")
+    _run_stack(cuda_device, w.hidden, w.intermediate, w.vocab, w.layers, w.S, w.C, w.d_kv, w.eps,
+               check_layers=[0, w.layers - 2], n_rows=16)
+
+
+def test_nccl_allgather_single_rank(cuda_device):
+    """The NCCL path of a11 through the C ABI (dlopen, comm init, in-place all-gather, destroy) at
+    world size 1 -- the only size a one-GPU box allows; N > 1 runs under torchrun."""
+    uid = _mom.nccl_get_unique_id()
+    comm = _mom.nccl_comm_init(1, uid, 0)
+    rows = synth.hidden(128, 256, cuda_device, torch.bfloat16)
+    ref = rows.clone()
+    _mom.allgather_rows(rows, 128, comm, 0, 1)
+    torch.cuda.synchronize()
+    _mom.nccl_comm_destroy(comm)
+    assert torch.equal(rows, ref)

@@ -1,0 +1,85 @@
+"""World-size-2 CPU (gloo) test of the token-sharded multi-GPU host logic:
+shard plan, last-token owner, and gather order.  Each rank computes its shard's rows with the
+ORACLE (the CUDA path needs GPUs and NCCL; its in-place all-gather is exercised on the GPU), the
+rows are all-gathered in rank order, and the result must equal the unsharded computation
+bitwise (rows are independent) -- including a padded (non-divisible) S."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2504_12526_b200.stack import last_token_owner, shard_rows
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _inputs(S, d, I):
+    r = np.random.default_rng(5)
+    x = r.standard_normal((S, d)).astype(np.float32)
+    wg = (r.standard_normal((I, d)) * 0.2).astype(np.float32)
+    wu = (r.standard_normal((I, d)) * 0.2).astype(np.float32)
+    wd = (r.standard_normal((d, I)) * 0.2).astype(np.float32)
+    return x, wg, wu, wd
+
+
+def _worker(rank, world, port, S, d, I, C, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x, wg, wu, wd = _inputs(S, d, I)
+        start, per, padded = shard_rows(S, world, rank)
+        xp = np.zeros((padded, d), np.float32)
+        xp[:S] = x
+        mine = oracle.mlp_minseq(xp[start:start + per], xp[start:start + per], wg, wu, wd, C=C, nthreads=1)
+        parts = [torch.empty((per, d), dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(mine))
+        gathered = torch.cat(parts).numpy()[:S]
+        owner = last_token_owner(S, world)
+        q.put((rank, gathered.tobytes(), owner, start, per, padded))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("S", [64, 67])
+def test_token_shard_gather_equals_unsharded(S):
+    world, d, I, C = 2, 16, 24, 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, S, d, I, C, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    x, wg, wu, wd = _inputs(S, d, I)
+    ref = oracle.mlp_minseq(x, x, wg, wu, wd, C=S)
+    res.sort()
+    for rank, blob, owner, start, per, padded in res:
+        assert blob == ref.tobytes(), rank
+        assert owner == (S - 1) // per and start == rank * per and padded == per * world
+
+
+def test_shard_plan_edges():
+    assert shard_rows(455000, 8, 7) == (7 * 56875, 56875, 455000)
+    assert shard_rows(10, 4, 3) == (9, 3, 12)
+    assert last_token_owner(455000, 8) == 7
+    assert last_token_owner(10, 4) == 3
+    assert last_token_owner(9, 4) == 2  # per = 3: rows 6..8 on rank 2, rank 3 holds only padding
+    with pytest.raises(ValueError):
+        shard_rows(10, 0, 0)
