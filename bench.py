@@ -185,13 +185,18 @@ class Workload:
         return self.out[self.rank * self.S:(self.rank + 1) * self.S]
 
 
-def run_step(wl, compute, copy, launches):
-    """One pass of the hot path, enqueued on `compute` (MLP, head) and `copy` (KV copies)."""
+def run_step(wl, compute, copy, launches, x_host=None, h2d=None):
+    """One pass of the hot path, enqueued on `compute` (MLP, head) and `copy` (KV copies).
+    With x_host (e2e): the input rows are streamed from pinned host memory on `h2d`, one
+    mini-sequence at a time, overlapping the MLP (mom_mlp_minseq_fwd_from_host)."""
     from paper_2504_12526_b200 import _mom
     copy.wait_stream(compute)
     _mom.kv_offload(wl.kv, wl.kv_host, compute, copy)                                   # a9
     wg, wu, wd = wl.w0
-    _mom.mlp_minseq_fwd(wl.x, wl.x, wg, wu, wd, wl.shard, wl.C, wl.ws, compute)         # a1-a4
+    if x_host is None:
+        _mom.mlp_minseq_fwd(wl.x, wl.x, wg, wu, wd, wl.shard, wl.C, wl.ws, compute)     # a1-a4
+    else:
+        _mom.mlp_minseq_fwd_from_host(x_host, wl.x, wl.x, wg, wu, wd, wl.shard, wl.C, wl.ws, compute, h2d)
     launches[0] += 2 * wl.M
     if wl.world > 1:
         _mom.allgather_rows(wl.out, wl.S, wl.comm, wl.rank, wl.world, compute)           # a11
@@ -363,9 +368,9 @@ def run_mine(args):
         e1 = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(compute):
             e0.record(compute)
+            h2d = torch.cuda.Stream(device)
             for _ in range(args.steps):
-                wl.x.copy_(x_host, non_blocking=True)
-                run_step(wl, compute, copy, [0])
+                run_step(wl, compute, copy, [0], x_host=x_host, h2d=h2d)
                 if wl.owns_last:
                     lg_host.copy_(wl.logits, non_blocking=True)
                     am_host.copy_(wl.argmax, non_blocking=True)

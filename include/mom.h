@@ -101,6 +101,20 @@ mom_status_t mom_mlp_minseq_fwd(const void *x, const void *residual, const void 
                                 mom_dtype_t dt, void *workspace, size_t workspace_bytes,
                                 mom_stream_t stream);
 
+/* The same, with the MLP input in page-locked HOST memory (the end-to-end entry).  For each
+ * mini-sequence i the rows of A_i are copied x_host_pinned -> x (device [S, hidden]) on
+ * copy_stream, and `stream` waits for exactly those rows before computing O_i, so the PCIe
+ * transfer of A_{i+1} overlaps the tensor-core work on A_i (the partition of P:109 applied to
+ * the host->device input).  copy_stream first waits for work already queued on `stream`.
+ * residual may equal x (the usual x + MLP(x)).  x_host_pinned must be page-locked (checked);
+ * copy_stream must differ from stream.  Other arguments and errors as mom_mlp_minseq_fwd. */
+mom_status_t mom_mlp_minseq_fwd_from_host(const void *x_host_pinned, void *x, const void *residual,
+                                          const void *w_gate, const void *w_up, const void *w_down,
+                                          void *out, int64_t S, int64_t hidden, int64_t intermediate,
+                                          int64_t minseq_len, mom_dtype_t dt, void *workspace,
+                                          size_t workspace_bytes, mom_stream_t stream,
+                                          mom_stream_t copy_stream);
+
 /* ------------------------------------------------------------------------------------
  * a6. Final layer on the last token only.  Alg. 1: A_last = A[:, -1, :]
  * (pass x + (S-1)*hidden), O_last = MLP(A_last) (+ residual_last if non-NULL).

@@ -16,6 +16,7 @@ from ._mom import (  # noqa: F401
     lm_head_last,
     mlp_last_token,
     mlp_minseq_fwd,
+    mlp_minseq_fwd_from_host,
     mlp_minseq_workspace_bytes,
     nccl_comm_destroy,
     nccl_comm_init,

@@ -25,6 +25,8 @@ SIGNATURES = {
     "mom_plan_minseq": (_i64, [_i64, _i64, _p, _p, _i64]),
     "mom_mlp_minseq_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64, _i32]),
     "mom_mlp_minseq_fwd": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i32, _p, _sz, _p]),
+    "mom_mlp_minseq_fwd_from_host": (_i32, [_p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i32, _p, _sz, _p,
+                                            _p]),
     "mom_mlp_last_token_workspace_bytes": (_sz, [_i64]),
     "mom_mlp_last_token": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _p, _sz, _p]),
     "mom_lm_head_workspace_bytes": (_sz, [_i64]),
@@ -164,6 +166,25 @@ def mlp_minseq_fwd(x, residual, w_gate, w_up, w_down, out, minseq_len: int, work
     ws_bytes = workspace.numel() * workspace.element_size()
     _check(lib().mom_mlp_minseq_fwd(_ptr(x), _ptr(residual), _ptr(w_gate), _ptr(w_up), _ptr(w_down), _ptr(out),
                                     S, hidden, I, minseq_len, dt, _ptr(workspace), ws_bytes, _stream(stream)))
+    return out
+
+
+def mlp_minseq_fwd_from_host(x_host, x, residual, w_gate, w_up, w_down, out, minseq_len: int, workspace=None,
+                             stream=None, copy_stream=None):
+    """End-to-end entry: x_host (pinned) is streamed into x one mini-sequence at a time on
+    copy_stream while the MLP of the previous mini-sequence runs on stream."""
+    S, hidden = x.shape
+    I = w_gate.shape[0]
+    dt = _dt(x)
+    if workspace is None:
+        nbytes = lib().mom_mlp_minseq_workspace_bytes(S, hidden, I, minseq_len, dt)
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    if copy_stream is None:
+        raise ValueError("copy_stream is required")
+    ws_bytes = workspace.numel() * workspace.element_size()
+    _check(lib().mom_mlp_minseq_fwd_from_host(_ptr(x_host), _ptr(x), _ptr(residual), _ptr(w_gate), _ptr(w_up),
+                                              _ptr(w_down), _ptr(out), S, hidden, I, minseq_len, dt, _ptr(workspace),
+                                              ws_bytes, _stream(stream), _stream(copy_stream)))
     return out
 
 

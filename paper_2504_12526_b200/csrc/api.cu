@@ -122,6 +122,18 @@ struct ScopedTiming {
   }
 };
 
+mom_status_t check_pinned(const void *host, const char *who) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, host);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(MOM_ERR_INVALID_ARG, "%s: cannot query host pointer (%s)", who, cudaGetErrorName(e));
+  }
+  if (at.type != cudaMemoryTypeHost)
+    return fail(MOM_ERR_INVALID_ARG, "%s: host buffer is not page-locked (cudaHostAlloc / pin_memory)", who);
+  return MOM_OK;
+}
+
 int env_int(const char *name, int dflt) {
   const char *v = getenv(name);
   return (v && *v) ? atoi(v) : dflt;
@@ -172,77 +184,94 @@ size_t mom_mlp_minseq_workspace_bytes(int64_t S, int64_t hidden, int64_t interme
   return (b + 255) & ~static_cast<size_t>(255);
 }
 
-mom_status_t mom_mlp_minseq_fwd(const void *x, const void *residual, const void *w_gate, const void *w_up,
-                                const void *w_down, void *out, int64_t S, int64_t hidden, int64_t intermediate,
-                                int64_t C, mom_dtype_t dt, void *workspace, size_t workspace_bytes,
-                                mom_stream_t stream_) {
-  g_err[0] = 0;
-  if (!x || !w_gate || !w_up || !w_down || !out || !workspace)
-    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd: null pointer");
+}  // extern "C"
+
+namespace {
+
+mom_status_t validate_minseq(const char *who, const void *x, const void *residual, const void *w_gate,
+                             const void *w_up, const void *w_down, const void *out, int64_t S, int64_t hidden,
+                             int64_t intermediate, int64_t C, mom_dtype_t dt, const void *workspace,
+                             size_t workspace_bytes) {
+  if (!x || !w_gate || !w_up || !w_down || !out || !workspace) return fail(MOM_ERR_INVALID_ARG, "%s: null pointer", who);
   if (S < 1 || hidden < 1 || intermediate < 1 || C < 1)
-    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd: S, hidden, intermediate, minseq_len must be >= 1");
-  if (!valid_dtype(dt)) return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd: bad dtype %d", (int)dt);
+    return fail(MOM_ERR_INVALID_ARG, "%s: S, hidden, intermediate, minseq_len must be >= 1", who);
+  if (!valid_dtype(dt)) return fail(MOM_ERR_INVALID_ARG, "%s: bad dtype %d", who, (int)dt);
   const size_t w = dtype_bytes(dt);
   if ((hidden * w) % 16 || (intermediate * w) % 16)
-    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd: row pitch must be a multiple of 16 bytes");
+    return fail(MOM_ERR_INVALID_ARG, "%s: row pitch must be a multiple of 16 bytes", who);
   if (!aligned16(x) || !aligned16(residual) || !aligned16(w_gate) || !aligned16(w_up) || !aligned16(w_down) ||
       !aligned16(out) || !aligned16(workspace))
-    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd: pointers must be 16-byte aligned");
+    return fail(MOM_ERR_INVALID_ARG, "%s: pointers must be 16-byte aligned", who);
   if (S > INT32_MAX || hidden > INT32_MAX || intermediate > INT32_MAX)
-    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd: dimension exceeds int32");
+    return fail(MOM_ERR_INVALID_ARG, "%s: dimension exceeds int32", who);
   const size_t act_bytes = static_cast<size_t>(S) * hidden * w;
   if (partial_overlap(out, act_bytes, x, act_bytes) || partial_overlap(out, act_bytes, residual, act_bytes))
-    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd: out partially overlaps x or residual");
+    return fail(MOM_ERR_INVALID_ARG, "%s: out partially overlaps x or residual", who);
   const size_t need = mom_mlp_minseq_workspace_bytes(S, hidden, intermediate, C, dt);
   if (workspace_bytes < need)
-    return fail(MOM_ERR_WORKSPACE, "mom_mlp_minseq_fwd: workspace %zu < required %zu bytes", workspace_bytes, need);
+    return fail(MOM_ERR_WORKSPACE, "%s: workspace %zu < required %zu bytes", who, workspace_bytes, need);
+  return MOM_OK;
+}
 
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+// Alg. 1 P:109-113.  When x_host is non-null, mini-sequence i's rows are first copied host->device
+// (x_host -> x) on `copy`, and `stream` waits for exactly those rows before running MLP(A_i): the
+// transfer of A_{i+1} overlaps the tensor-core work on A_i.
+mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate, const void *w_up,
+                        const void *w_down, void *out, int64_t S, int64_t hidden, int64_t intermediate, int64_t C,
+                        mom_dtype_t dt, void *workspace, cudaStream_t stream, const void *x_host,
+                        cudaStream_t copy) {
   int num_sms = 0;
   if (num_sms_current(&num_sms) != 0) return fail(MOM_ERR_CUDA, "mom_mlp_minseq_fwd: no CUDA device");
   const int64_t M = (S + C - 1) / C;  // Alg. 1
-
-  if (dt == MOM_F32) {
-    for (int64_t i = 0; i < M; ++i) {  // Alg. 1: for i = 1..M
-      const int64_t r0 = i * C;
-      const int64_t rows = (r0 + C < S) ? C : S - r0;
-      const float *xi = static_cast<const float *>(x) + r0 * hidden;
-      const float *ri = residual ? static_cast<const float *>(residual) + r0 * hidden : nullptr;
-      float *oi = static_cast<float *>(out) + r0 * hidden;  // concat: O_i lands at its rows
-      float *h = static_cast<float *>(workspace);
-      cudaError_t e;
-      {
-        ScopedTiming tm(stream, 2);
-        e = mom::launch_phase_a_f32(xi, static_cast<const float *>(w_gate),
-                                              static_cast<const float *>(w_up), h, (int)rows, (int)hidden,
-                                              (int)intermediate, stream);
-      }
-      if (e != cudaSuccess) return cuda_fail(e, "phase A (f32)");
-      {
-        ScopedTiming tm(stream, 3);
-        e = mom::launch_phase_b_f32(h, static_cast<const float *>(w_down), ri, oi, (int)rows, (int)hidden,
-                                    (int)intermediate, stream);
-      }
-      if (e != cudaSuccess) return cuda_fail(e, "phase B (f32)");
-    }
-    return MOM_OK;
-  }
-
-  // bf16 tcgen05 path
+  const size_t w = dtype_bytes(dt);
   const int cta_group = env_int("MOM_CTA_GROUP", 2) == 1 ? 1 : 2;
   const uint32_t group_a = static_cast<uint32_t>(env_int("MOM_GROUP_M_A", 0));
   const uint32_t group_b = static_cast<uint32_t>(env_int("MOM_GROUP_M_B", 0));
   CUtensorMap tm_wg, tm_wu, tm_wd;
   mom_status_t st;
-  if ((st = make_tmap(&tm_wg, w_gate, intermediate, hidden, "w_gate")) != MOM_OK) return st;
-  if ((st = make_tmap(&tm_wu, w_up, intermediate, hidden, "w_up")) != MOM_OK) return st;
-  if ((st = make_tmap(&tm_wd, w_down, hidden, intermediate, "w_down")) != MOM_OK) return st;
+  if (dt == MOM_BF16) {
+    if ((st = make_tmap(&tm_wg, w_gate, intermediate, hidden, "w_gate")) != MOM_OK) return st;
+    if ((st = make_tmap(&tm_wu, w_up, intermediate, hidden, "w_up")) != MOM_OK) return st;
+    if ((st = make_tmap(&tm_wd, w_down, hidden, intermediate, "w_down")) != MOM_OK) return st;
+  }
   for (int64_t i = 0; i < M; ++i) {  // Alg. 1: for i = 1..M (sequential on `stream`)
     const int64_t r0 = i * C;
     const int64_t rows = (r0 + C < S) ? C : S - r0;
-    const __nv_bfloat16 *xi = static_cast<const __nv_bfloat16 *>(x) + r0 * hidden;
-    const __nv_bfloat16 *ri = residual ? static_cast<const __nv_bfloat16 *>(residual) + r0 * hidden : nullptr;
-    __nv_bfloat16 *oi = static_cast<__nv_bfloat16 *>(out) + r0 * hidden;
+    const size_t off = static_cast<size_t>(r0) * hidden * w;  // byte offset of A_i / O_i
+    cudaError_t e;
+    if (x_host) {
+      e = cudaMemcpyAsync(const_cast<char *>(static_cast<const char *>(x)) + off,
+                          static_cast<const char *>(x_host) + off, static_cast<size_t>(rows) * hidden * w,
+                          cudaMemcpyHostToDevice, copy);
+      if (e != cudaSuccess) return cuda_fail(e, "mini-sequence H2D");
+      cudaEvent_t landed;
+      if ((e = cudaEventCreateWithFlags(&landed, cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "event create");
+      e = cudaEventRecord(landed, copy);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, landed, 0);
+      cudaEventDestroy(landed);
+      if (e != cudaSuccess) return cuda_fail(e, "mini-sequence H2D ordering");
+    }
+    const void *xi = static_cast<const char *>(x) + off;
+    const void *ri = residual ? static_cast<const char *>(residual) + off : nullptr;
+    void *oi = static_cast<char *>(out) + off;  // concat: O_i lands at its rows
+    if (dt == MOM_F32) {
+      float *h = static_cast<float *>(workspace);
+      {
+        ScopedTiming tm(stream, 2);
+        e = mom::launch_phase_a_f32(static_cast<const float *>(xi), static_cast<const float *>(w_gate),
+                                    static_cast<const float *>(w_up), h, (int)rows, (int)hidden, (int)intermediate,
+                                    stream);
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "phase A (f32)");
+      {
+        ScopedTiming tm(stream, 3);
+        e = mom::launch_phase_b_f32(h, static_cast<const float *>(w_down), static_cast<const float *>(ri),
+                                    static_cast<float *>(oi), (int)rows, (int)hidden, (int)intermediate, stream);
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "phase B (f32)");
+      continue;
+    }
     __nv_bfloat16 *h = static_cast<__nv_bfloat16 *>(workspace);
     // Per-mini-sequence maps: the row bound is C_i, so TMA zero-fills loads past the end of
     // this mini-sequence and no tile reads another mini-sequence's rows.
@@ -254,7 +283,6 @@ mom_status_t mom_mlp_minseq_fwd(const void *x, const void *residual, const void 
     a.rows = (uint32_t)rows; a.n_out = (uint32_t)intermediate; a.k = (uint32_t)hidden;
     a.out = h; a.residual = nullptr; a.ld_out = (uint32_t)intermediate;
     a.cta_group = cta_group; a.group_m = group_a; a.num_sms = num_sms;
-    cudaError_t e;
     {
       ScopedTiming tm(stream, 0);
       e = mom::launch_phase_a_tc(a, stream);  // H_i = Swish(A_i Wg^T) (.) A_i Wu^T
@@ -263,7 +291,8 @@ mom_status_t mom_mlp_minseq_fwd(const void *x, const void *residual, const void 
     mom::TcPhaseArgs b{};
     b.tm_a = &tm_h; b.tm_b0 = &tm_wd; b.tm_b1 = &tm_wd;
     b.rows = (uint32_t)rows; b.n_out = (uint32_t)hidden; b.k = (uint32_t)intermediate;
-    b.out = oi; b.residual = ri; b.ld_out = (uint32_t)hidden;
+    b.out = static_cast<__nv_bfloat16 *>(oi); b.residual = static_cast<const __nv_bfloat16 *>(ri);
+    b.ld_out = (uint32_t)hidden;
     b.cta_group = cta_group; b.group_m = group_b; b.num_sms = num_sms;
     {
       ScopedTiming tm(stream, 1);
@@ -272,6 +301,47 @@ mom_status_t mom_mlp_minseq_fwd(const void *x, const void *residual, const void 
     if (e != cudaSuccess) return cuda_fail(e, "phase B (tcgen05)");
   }
   return MOM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+mom_status_t mom_mlp_minseq_fwd(const void *x, const void *residual, const void *w_gate, const void *w_up,
+                                const void *w_down, void *out, int64_t S, int64_t hidden, int64_t intermediate,
+                                int64_t C, mom_dtype_t dt, void *workspace, size_t workspace_bytes,
+                                mom_stream_t stream) {
+  g_err[0] = 0;
+  mom_status_t st = validate_minseq("mom_mlp_minseq_fwd", x, residual, w_gate, w_up, w_down, out, S, hidden,
+                                    intermediate, C, dt, workspace, workspace_bytes);
+  if (st != MOM_OK) return st;
+  return run_minseq(x, residual, w_gate, w_up, w_down, out, S, hidden, intermediate, C, dt, workspace,
+                    static_cast<cudaStream_t>(stream), nullptr, nullptr);
+}
+
+mom_status_t mom_mlp_minseq_fwd_from_host(const void *x_host_pinned, void *x, const void *residual,
+                                          const void *w_gate, const void *w_up, const void *w_down, void *out,
+                                          int64_t S, int64_t hidden, int64_t intermediate, int64_t C,
+                                          mom_dtype_t dt, void *workspace, size_t workspace_bytes,
+                                          mom_stream_t stream, mom_stream_t copy_stream) {
+  g_err[0] = 0;
+  if (!x_host_pinned) return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd_from_host: null host pointer");
+  mom_status_t st = validate_minseq("mom_mlp_minseq_fwd_from_host", x, residual, w_gate, w_up, w_down, out, S,
+                                    hidden, intermediate, C, dt, workspace, workspace_bytes);
+  if (st != MOM_OK) return st;
+  if ((st = check_pinned(x_host_pinned, "mom_mlp_minseq_fwd_from_host")) != MOM_OK) return st;
+  if (copy_stream == stream) return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd_from_host: copy_stream must differ from stream");
+  cudaStream_t s = static_cast<cudaStream_t>(stream), cp = static_cast<cudaStream_t>(copy_stream);
+  // the copy stream must not start writing x before earlier work on `stream` is done with it
+  cudaEvent_t ready;
+  cudaError_t e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  if (e != cudaSuccess) return cuda_fail(e, "event create");
+  e = cudaEventRecord(ready, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cp, ready, 0);
+  cudaEventDestroy(ready);
+  if (e != cudaSuccess) return cuda_fail(e, "stream ordering");
+  return run_minseq(x, residual, w_gate, w_up, w_down, out, S, hidden, intermediate, C, dt, workspace, s,
+                    x_host_pinned, cp);
 }
 
 size_t mom_mlp_last_token_workspace_bytes(int64_t intermediate) {
@@ -348,18 +418,6 @@ mom_status_t mom_lm_head_last(const void *h_last, const void *norm_gain, float e
                                       static_cast<unsigned long long *>(workspace), (int)hidden, (int)vocab,
                                       dt == MOM_BF16, num_sms, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "lm head");
-  return MOM_OK;
-}
-
-static mom_status_t check_pinned(const void *host, const char *who) {
-  cudaPointerAttributes at;
-  cudaError_t e = cudaPointerGetAttributes(&at, host);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return fail(MOM_ERR_INVALID_ARG, "%s: cannot query host pointer (%s)", who, cudaGetErrorName(e));
-  }
-  if (at.type != cudaMemoryTypeHost)
-    return fail(MOM_ERR_INVALID_ARG, "%s: host buffer is not page-locked (cudaHostAlloc / pin_memory)", who);
   return MOM_OK;
 }
 

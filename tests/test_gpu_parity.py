@@ -239,3 +239,21 @@ def test_workspace_too_small_is_reported(cuda_device):
     with pytest.raises(_mom.MomError) as ei:
         _mom.mlp_minseq_fwd(*g, torch.empty_like(g[0]), 128, workspace=ws)
     assert ei.value.status == _mom.MOM_ERR_WORKSPACE
+
+
+def test_from_host_streamed_equals_device_input(cuda_device):
+    """mom_mlp_minseq_fwd_from_host (per-mini-sequence H2D overlapped with the MLP) gives the
+    bitwise result of the device-input call, for ragged mini-sequences."""
+    S, d, I, C = 1000, 256, 688, 300
+    (x, res, wg, wu, wd), g = _mlp_inputs(S, d, I, torch.bfloat16, cuda_device, residual=False)
+    ref = _run_fwd(g[0], g[0], *g[2:], C=C)
+    x_host = x.pin_memory()
+    x_dev = torch.zeros_like(g[0])
+    out = torch.empty_like(g[0])
+    cp = torch.cuda.Stream()
+    _mom.mlp_minseq_fwd_from_host(x_host, x_dev, x_dev, g[2], g[3], g[4], out, C, copy_stream=cp)
+    torch.cuda.synchronize()
+    assert torch.equal(x_dev, g[0])
+    assert torch.equal(out, ref)
+    with pytest.raises(_mom.MomError):  # pageable host memory is rejected
+        _mom.mlp_minseq_fwd_from_host(x.clone(), x_dev, x_dev, g[2], g[3], g[4], out, C, copy_stream=cp)
