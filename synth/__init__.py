@@ -42,20 +42,21 @@ class Workload:
     d_kv: int
     dtype: str        # "f32" | "bf16"
     eps: float = 1e-5
+    minseq_len: int = 0  # explicit C (the paper's chunk 8192); 0 -> C = ceil(S / M)
 
     @property
     def C(self) -> int:
-        return (self.S + self.M - 1) // self.M
+        return self.minseq_len or (self.S + self.M - 1) // self.M
 
 
-# BASELINE.json "configs" (index = position in that list).  M for configs 3-5 follows
-# the paper's chunk size 8192: M = ceil(S / 8192).
+# BASELINE.json "configs" (index = position in that list).  Configs 3-5 use the paper's chunk
+# size C = 8192: M = ceil(S / 8192) = 16 / 19 (tail 7544) / 56 (tail 4440).
 CONFIGS = {
     0: Workload("cfg1-f32-d256-I688-S1024-M4-V1000", 256, 688, 1024, 4, 1000, 1, 64, "f32"),
     1: Workload("cfg2-llama3-8b-mlp-S65536-M8", 4096, 14336, 65536, 8, 128256, 32, 1024, "bf16"),
-    2: Workload("cfg3-qwen2.5-7b-28L-S131072", 3584, 18944, 131072, 16, 152064, 28, 512, "bf16", 1e-6),
-    3: Workload("cfg4-mistral-nemo-12b-40L-S155000", 5120, 14336, 155000, 19, 131072, 40, 1024, "bf16"),
-    4: Workload("cfg5-llama3-8b-32L-S455000", 4096, 14336, 455000, 56, 128256, 32, 1024, "bf16"),
+    2: Workload("cfg3-qwen2.5-7b-28L-S131072", 3584, 18944, 131072, 16, 152064, 28, 512, "bf16", 1e-6, 8192),
+    3: Workload("cfg4-mistral-nemo-12b-40L-S155000", 5120, 14336, 155000, 19, 131072, 40, 1024, "bf16", 1e-5, 8192),
+    4: Workload("cfg5-llama3-8b-32L-S455000", 4096, 14336, 455000, 56, 128256, 32, 1024, "bf16", 1e-5, 8192),
 }
 
 
