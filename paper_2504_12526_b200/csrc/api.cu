@@ -227,6 +227,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
   const int cta_group = env_int("MOM_CTA_GROUP", 2) == 1 ? 1 : 2;
   const uint32_t group_a = static_cast<uint32_t>(env_int("MOM_GROUP_M_A", 0));
   const uint32_t group_b = static_cast<uint32_t>(env_int("MOM_GROUP_M_B", 0));
+  const uint32_t policy = static_cast<uint32_t>(env_int("MOM_TMA_POLICY", 0));
   CUtensorMap tm_wg, tm_wu, tm_wd;
   mom_status_t st;
   if (dt == MOM_BF16) {
@@ -282,7 +283,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     a.tm_a = &tm_x; a.tm_b0 = &tm_wg; a.tm_b1 = &tm_wu;
     a.rows = (uint32_t)rows; a.n_out = (uint32_t)intermediate; a.k = (uint32_t)hidden;
     a.out = h; a.residual = nullptr; a.ld_out = (uint32_t)intermediate;
-    a.cta_group = cta_group; a.group_m = group_a; a.num_sms = num_sms;
+    a.cta_group = cta_group; a.group_m = group_a; a.policy = policy; a.num_sms = num_sms;
     {
       ScopedTiming tm(stream, 0);
       e = mom::launch_phase_a_tc(a, stream);  // H_i = Swish(A_i Wg^T) (.) A_i Wu^T
@@ -293,7 +294,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     b.rows = (uint32_t)rows; b.n_out = (uint32_t)hidden; b.k = (uint32_t)intermediate;
     b.out = static_cast<__nv_bfloat16 *>(oi); b.residual = static_cast<const __nv_bfloat16 *>(ri);
     b.ld_out = (uint32_t)hidden;
-    b.cta_group = cta_group; b.group_m = group_b; b.num_sms = num_sms;
+    b.cta_group = cta_group; b.group_m = group_b; b.policy = policy; b.num_sms = num_sms;
     {
       ScopedTiming tm(stream, 1);
       e = mom::launch_phase_b_tc(b, stream);  // O_i = R_i + H_i Wd^T, written at rows r0..

@@ -21,6 +21,7 @@ struct TcPhaseArgs {
   uint32_t ld_out;           // row pitch of out/residual in elements
   int cta_group;             // 1 or 2
   uint32_t group_m;          // raster group (0 = default)
+  uint32_t policy;           // TMA L2 cache policy variant (0 = default)
   int num_sms;
 };
 cudaError_t launch_phase_a_tc(const TcPhaseArgs &a, cudaStream_t stream);

@@ -66,6 +66,7 @@ struct Params {
   uint32_t m_tiles;      // ceil(rows / (BM*CG))
   uint32_t n_tiles;      // ceil(n_out / tile_n)
   uint32_t group_m;      // raster: M tiles per group (N iterates inside a group)
+  uint32_t policy;       // TMA L2 policy: 0 reuse-aware (default), 1 all evict_normal, 2 A evict_first
   // epilogue
   __nv_bfloat16 *out;            // phase A: H_i [rows, I]; phase B: out rows [rows, d]
   const __nv_bfloat16 *residual; // phase B only, may be null
@@ -140,8 +141,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     // ======================= TMA producer =======================
     if (lane == 0) {
-      const uint64_t pol_a = PHASE_A ? ptx::policy_evict_last() : ptx::policy_evict_normal();
-      const uint64_t pol_b = PHASE_A ? ptx::policy_evict_normal() : ptx::policy_evict_last();
+      const uint64_t pol_a = p.policy == 1 ? ptx::policy_evict_normal()
+                             : p.policy == 2 ? ptx::policy_evict_first()
+                             : (PHASE_A ? ptx::policy_evict_last() : ptx::policy_evict_normal());
+      const uint64_t pol_b = p.policy == 1 ? ptx::policy_evict_normal()
+                             : (PHASE_A ? ptx::policy_evict_normal() : ptx::policy_evict_last());
       const uint32_t full_leader0 = (CG == 2) ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : ptx::smem_u32(&full[0]);
       uint32_t stage = 0, phase = 0;
       for (uint32_t t = cluster_id; t < num_tiles; t += num_clusters) {
@@ -342,11 +346,12 @@ cudaError_t launch_phase_a_tc(const TcPhaseArgs &a, cudaStream_t stream) {
   p.k = a.k;
   p.m_tiles = (a.rows + tc::BM * a.cta_group - 1) / (tc::BM * a.cta_group);
   p.n_tiles = (a.n_out + tc::BHALF - 1) / tc::BHALF;
-  p.group_m = a.group_m ? a.group_m : p.m_tiles;
+  p.group_m = a.group_m ? a.group_m : 16;  // 16 x 256 rows: X rows of a group stay in L2 (energy sweep r1)
   if (p.group_m > p.m_tiles) p.group_m = p.m_tiles;
   p.out = a.out;
   p.residual = nullptr;
   p.ld_out = a.ld_out;
+  p.policy = a.policy;
   if (a.cta_group == 2) return tc::launch<2, true>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
   return tc::launch<1, true>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
 }
@@ -363,6 +368,7 @@ cudaError_t launch_phase_b_tc(const TcPhaseArgs &a, cudaStream_t stream) {
   p.out = a.out;
   p.residual = a.residual;
   p.ld_out = a.ld_out;
+  p.policy = a.policy;
   if (a.cta_group == 2) return tc::launch<2, false>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
   return tc::launch<1, false>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
 }
