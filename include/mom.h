@@ -116,6 +116,28 @@ mom_status_t mom_mlp_minseq_fwd_from_host(const void *x_host_pinned, void *x, co
                                           mom_stream_t copy_stream);
 
 /* ------------------------------------------------------------------------------------
+ * f3. The per-layer RMSNorm folded into the mini-sequence MLP: the Llama
+ * block's MLP half  out = x + MLP(RMSNorm(x) (.) g)  (RMSNorm S:126) without
+ * writing the normed [S, d] tensor.  Since (RMSNorm(x) (.) g) W^T = r * x (W diag(g))^T with
+ * r = 1/sqrt(mean(x^2) + eps) per row:
+ *   mom_fold_norm_gain           once per layer: w_folded[j, k] = bf16(w[j, k] * g[k]) for W_gate
+ *                                and W_up ([rows, cols] = [I, d]; cols % 8 == 0; may be in place)
+ *   mom_mlp_minseq_rmsnorm_fwd   per mini-sequence: r of its rows (one pass over C*d elements),
+ *                                then phase A scales the fp32 gate/up accumulators by r before the
+ *                                SiLU; phase B adds the residual x.  out may alias x.
+ * bf16 only (MOM_ERR_UNSUPPORTED otherwise).  Workspace: one H_i plus C fp32 scales.
+ * ---------------------------------------------------------------------------------- */
+mom_status_t mom_fold_norm_gain(const void *w, const void *norm_gain, void *w_folded, int64_t rows,
+                                int64_t cols, mom_dtype_t dt, mom_stream_t stream);
+size_t mom_mlp_minseq_rmsnorm_workspace_bytes(int64_t S, int64_t hidden, int64_t intermediate,
+                                              int64_t minseq_len, mom_dtype_t dt);
+mom_status_t mom_mlp_minseq_rmsnorm_fwd(const void *x, const void *w_gate_folded,
+                                        const void *w_up_folded, const void *w_down, void *out,
+                                        int64_t S, int64_t hidden, int64_t intermediate,
+                                        int64_t minseq_len, float eps, mom_dtype_t dt,
+                                        void *workspace, size_t workspace_bytes, mom_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
  * a6. Final layer on the last token only.  Alg. 1: A_last = A[:, -1, :]
  * (pass x + (S-1)*hidden), O_last = MLP(A_last) (+ residual_last if non-NULL).
  * HBM-bound GEMV pair: h = Swish(W_gate x) (.) (W_up x) kept in fp32 in `workspace`, then

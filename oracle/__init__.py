@@ -53,6 +53,8 @@ def _load():
         lib.oracle_mlp_rows.argtypes = [p, p, p, p, p, p, i64, i64, i64, p, i32]
         lib.oracle_mlp_minseq.restype = i32
         lib.oracle_mlp_minseq.argtypes = [p, p, p, p, p, i64, i64, i64, i64, p, i32]
+        lib.oracle_mlp_norm_rows.restype = i32
+        lib.oracle_mlp_norm_rows.argtypes = [p, p, dbl, p, p, p, p, i64, i64, i64, p, i32]
         lib.oracle_rmsnorm.restype = i32
         lib.oracle_rmsnorm.argtypes = [p, p, dbl, i64, p]
         lib.oracle_lm_head.restype = i32
@@ -128,6 +130,23 @@ def mlp_rows(x, residual, w_gate, w_up, w_down, rows, nthreads: int | None = Non
                              _ptr(rows), rows.size, d, I, _ptr(out), nthreads or default_threads())
     if rc != 0:
         raise RuntimeError("oracle_mlp_rows failed")
+    return out
+
+
+def mlp_norm_rows(x, gain, eps: float, w_gate, w_up, w_down, rows, nthreads: int | None = None) -> np.ndarray:
+    """f3: out = x + MLP(RMSNorm(x) * gain) on the listed rows, float64 [len(rows), d]."""
+    lib = _load()
+    x, g = _f32(x), _f32(gain)
+    wg, wu, wd = _f32(w_gate), _f32(w_up), _f32(w_down)
+    S, d = x.shape
+    I = wg.shape[0]
+    assert g.shape == (d,) and wg.shape == (I, d) and wu.shape == (I, d) and wd.shape == (d, I)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.zeros((rows.size, d), np.float64)
+    rc = lib.oracle_mlp_norm_rows(_ptr(x), _ptr(g), float(eps), _ptr(wg), _ptr(wu), _ptr(wd), _ptr(rows),
+                                  rows.size, d, I, _ptr(out), nthreads or default_threads())
+    if rc != 0:
+        raise RuntimeError("oracle_mlp_norm_rows failed")
     return out
 
 

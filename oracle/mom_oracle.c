@@ -185,6 +185,87 @@ int oracle_mlp_minseq(const float *x, const float *residual,
     return rc;
 }
 
+/* f3: the Llama pre-norm block's MLP half ("x + mlp(norm(x))"),
+ *   xn = RMSNorm(x) (.) gain,  RMSNorm(x)_k = x_k / sqrt(mean(x^2) + eps)
+ *   out = x + MLP(xn)
+ * evaluated exactly in that order, row by row, float64. */
+typedef struct {
+    const float *x, *gain, *wg, *wu, *wd;
+    double eps;
+    const int64_t *rows;
+    int64_t d, I;
+    double *out;
+    int64_t t_begin, t_end;
+    int status;
+} norm_job_t;
+
+static void *norm_worker(void *arg)
+{
+    norm_job_t *jb = (norm_job_t *)arg;
+    double *xn = (double *)malloc(sizeof(double) * (size_t)jb->d);
+    double *h = (double *)malloc(sizeof(double) * (size_t)jb->I);
+    if (!xn || !h) { free(xn); free(h); jb->status = -1; return NULL; }
+    for (int64_t t = jb->t_begin; t < jb->t_end; ++t) {
+        const float *x = jb->x + jb->rows[t] * jb->d;
+        double ss = 0.0;
+        for (int64_t k = 0; k < jb->d; ++k) ss = ss + (double)x[k] * (double)x[k];
+        double inv = 1.0 / sqrt(ss / (double)jb->d + jb->eps);
+        for (int64_t k = 0; k < jb->d; ++k) xn[k] = (double)x[k] * inv * (double)jb->gain[k];
+        for (int64_t j = 0; j < jb->I; ++j) {
+            const float *wg_j = jb->wg + j * jb->d, *wu_j = jb->wu + j * jb->d;
+            double g = 0.0, u = 0.0;
+            for (int64_t k = 0; k < jb->d; ++k) {
+                g = g + xn[k] * (double)wg_j[k];
+                u = u + xn[k] * (double)wu_j[k];
+            }
+            h[j] = swish(g) * u;
+        }
+        double *o = jb->out + t * jb->d;
+        for (int64_t c = 0; c < jb->d; ++c) {
+            const float *wd_c = jb->wd + c * jb->I;
+            double acc = 0.0;
+            for (int64_t j = 0; j < jb->I; ++j) acc = acc + h[j] * (double)wd_c[j];
+            o[c] = (double)x[c] + acc;
+        }
+    }
+    free(xn); free(h);
+    jb->status = 0;
+    return NULL;
+}
+
+int oracle_mlp_norm_rows(const float *x, const float *gain, double eps, const float *w_gate,
+                         const float *w_up, const float *w_down, const int64_t *rows, int64_t n_rows,
+                         int64_t d, int64_t I, double *out, int nthreads)
+{
+    if (!x || !gain || !w_gate || !w_up || !w_down || !out || (n_rows > 0 && !rows)) return -1;
+    if (d < 1 || I < 1 || n_rows < 0 || eps < 0.0) return -1;
+    if (n_rows == 0) return 0;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > n_rows) nthreads = (int)n_rows;
+    norm_job_t *jobs = (norm_job_t *)calloc((size_t)nthreads, sizeof(norm_job_t));
+    pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+    int *started = (int *)calloc((size_t)nthreads, sizeof(int));
+    if (!jobs || !th || !started) { free(jobs); free(th); free(started); return -1; }
+    int64_t per = (n_rows + nthreads - 1) / nthreads;
+    for (int t = 0; t < nthreads; ++t) {
+        norm_job_t *jb = &jobs[t];
+        jb->x = x; jb->gain = gain; jb->eps = eps; jb->wg = w_gate; jb->wu = w_up; jb->wd = w_down;
+        jb->rows = rows; jb->d = d; jb->I = I; jb->out = out;
+        jb->t_begin = (int64_t)t * per; if (jb->t_begin > n_rows) jb->t_begin = n_rows;
+        jb->t_end = jb->t_begin + per > n_rows ? n_rows : jb->t_begin + per;
+        jb->status = -2;
+    }
+    for (int t = 1; t < nthreads; ++t) started[t] = pthread_create(&th[t], NULL, norm_worker, &jobs[t]) == 0;
+    norm_worker(&jobs[0]);
+    for (int t = 1; t < nthreads; ++t) {
+        if (started[t]) pthread_join(th[t], NULL); else norm_worker(&jobs[t]);
+    }
+    int rc = 0;
+    for (int t = 0; t < nthreads; ++t) if (jobs[t].status != 0) rc = -1;
+    free(jobs); free(th); free(started);
+    return rc;
+}
+
 /* Final RMSNorm on one row (S:126 rmsnorm: y = x / sqrt(mean(x^2) + eps) (.) gain; applied
  * after slicing the last token).  gain may be NULL (= all ones). */
 int oracle_rmsnorm(const double *y, const float *gain, double eps, int64_t d, double *out)

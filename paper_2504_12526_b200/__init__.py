@@ -15,8 +15,10 @@ from ._mom import (  # noqa: F401
     lib,
     lm_head_last,
     mlp_last_token,
+    fold_norm_gain,
     mlp_minseq_fwd,
     mlp_minseq_fwd_from_host,
+    mlp_minseq_rmsnorm_fwd,
     mlp_minseq_workspace_bytes,
     nccl_comm_destroy,
     nccl_comm_init,

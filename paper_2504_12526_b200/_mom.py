@@ -27,6 +27,9 @@ SIGNATURES = {
     "mom_mlp_minseq_fwd": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i32, _p, _sz, _p]),
     "mom_mlp_minseq_fwd_from_host": (_i32, [_p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i32, _p, _sz, _p,
                                             _p]),
+    "mom_fold_norm_gain": (_i32, [_p, _p, _p, _i64, _i64, _i32, _p]),
+    "mom_mlp_minseq_rmsnorm_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64, _i32]),
+    "mom_mlp_minseq_rmsnorm_fwd": (_i32, [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _f32, _i32, _p, _sz, _p]),
     "mom_mlp_last_token_workspace_bytes": (_sz, [_i64]),
     "mom_mlp_last_token": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _p, _sz, _p]),
     "mom_lm_head_workspace_bytes": (_sz, [_i64]),
@@ -185,6 +188,29 @@ def mlp_minseq_fwd_from_host(x_host, x, residual, w_gate, w_up, w_down, out, min
     _check(lib().mom_mlp_minseq_fwd_from_host(_ptr(x_host), _ptr(x), _ptr(residual), _ptr(w_gate), _ptr(w_up),
                                               _ptr(w_down), _ptr(out), S, hidden, I, minseq_len, dt, _ptr(workspace),
                                               ws_bytes, _stream(stream), _stream(copy_stream)))
+    return out
+
+
+def fold_norm_gain(w, norm_gain, w_folded=None, stream=None):
+    """f3: w_folded = w * diag(norm_gain) (bf16), once per layer for W_gate and W_up."""
+    w_folded = torch.empty_like(w) if w_folded is None else w_folded
+    rows, cols = w.shape
+    _check(lib().mom_fold_norm_gain(_ptr(w), _ptr(norm_gain), _ptr(w_folded), rows, cols, _dt(w), _stream(stream)))
+    return w_folded
+
+
+def mlp_minseq_rmsnorm_fwd(x, w_gate_folded, w_up_folded, w_down, out, minseq_len: int, eps: float,
+                           workspace=None, stream=None):
+    """f3: out = x + MLP(RMSNorm(x) * g) with g folded into W_gate/W_up, per mini-sequence."""
+    S, hidden = x.shape
+    I = w_gate_folded.shape[0]
+    dt = _dt(x)
+    if workspace is None:
+        nbytes = lib().mom_mlp_minseq_rmsnorm_workspace_bytes(S, hidden, I, minseq_len, dt)
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    _check(lib().mom_mlp_minseq_rmsnorm_fwd(_ptr(x), _ptr(w_gate_folded), _ptr(w_up_folded), _ptr(w_down), _ptr(out),
+                                            S, hidden, I, minseq_len, float(eps), dt, _ptr(workspace),
+                                            workspace.numel() * workspace.element_size(), _stream(stream)))
     return out
 
 

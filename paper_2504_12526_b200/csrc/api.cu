@@ -219,7 +219,7 @@ mom_status_t validate_minseq(const char *who, const void *x, const void *residua
 mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate, const void *w_up,
                         const void *w_down, void *out, int64_t S, int64_t hidden, int64_t intermediate, int64_t C,
                         mom_dtype_t dt, void *workspace, cudaStream_t stream, const void *x_host,
-                        cudaStream_t copy) {
+                        cudaStream_t copy, const float *norm_eps = nullptr) {
   int num_sms = 0;
   if (num_sms_current(&num_sms) != 0) return fail(MOM_ERR_CUDA, "mom_mlp_minseq_fwd: no CUDA device");
   const int64_t M = (S + C - 1) / C;  // Alg. 1
@@ -284,6 +284,15 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     a.rows = (uint32_t)rows; a.n_out = (uint32_t)intermediate; a.k = (uint32_t)hidden;
     a.out = h; a.residual = nullptr; a.ld_out = (uint32_t)intermediate;
     a.cta_group = cta_group; a.group_m = group_a; a.policy = policy; a.num_sms = num_sms;
+    if (norm_eps) {
+      // folded RMSNorm (f3): 1/rms of this mini-sequence's rows, after H_i in the workspace
+      float *inv = reinterpret_cast<float *>(static_cast<char *>(workspace) +
+                                             mom_mlp_minseq_workspace_bytes(S, hidden, intermediate, C, dt));
+      e = mom::launch_row_inv_rms(static_cast<const __nv_bfloat16 *>(xi), inv, (int)rows, (int)hidden, *norm_eps,
+                                  num_sms, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "row 1/rms");
+      a.row_scale = inv;
+    }
     {
       ScopedTiming tm(stream, 0);
       e = mom::launch_phase_a_tc(a, stream);  // H_i = Swish(A_i Wg^T) (.) A_i Wu^T
@@ -343,6 +352,52 @@ mom_status_t mom_mlp_minseq_fwd_from_host(const void *x_host_pinned, void *x, co
   if (e != cudaSuccess) return cuda_fail(e, "stream ordering");
   return run_minseq(x, residual, w_gate, w_up, w_down, out, S, hidden, intermediate, C, dt, workspace, s,
                     x_host_pinned, cp);
+}
+
+mom_status_t mom_fold_norm_gain(const void *w, const void *norm_gain, void *w_folded, int64_t rows, int64_t cols,
+                                mom_dtype_t dt, mom_stream_t stream) {
+  g_err[0] = 0;
+  if (!w || !norm_gain || !w_folded) return fail(MOM_ERR_INVALID_ARG, "mom_fold_norm_gain: null pointer");
+  if (rows < 1 || cols < 1) return fail(MOM_ERR_INVALID_ARG, "mom_fold_norm_gain: sizes must be >= 1");
+  if (dt != MOM_BF16) return fail(MOM_ERR_UNSUPPORTED, "mom_fold_norm_gain: bf16 only");
+  if (cols % 8 || !aligned16(w) || !aligned16(norm_gain) || !aligned16(w_folded))
+    return fail(MOM_ERR_INVALID_ARG, "mom_fold_norm_gain: 16-byte alignment and cols %% 8 == 0 required");
+  if (partial_overlap(w, rows * cols * 2, w_folded, rows * cols * 2))
+    return fail(MOM_ERR_INVALID_ARG, "mom_fold_norm_gain: w_folded partially overlaps w");
+  int num_sms = 0;
+  if (num_sms_current(&num_sms) != 0) return fail(MOM_ERR_CUDA, "mom_fold_norm_gain: no CUDA device");
+  cudaError_t e = mom::launch_fold_gain(static_cast<const __nv_bfloat16 *>(w),
+                                        static_cast<const __nv_bfloat16 *>(norm_gain),
+                                        static_cast<__nv_bfloat16 *>(w_folded), rows, cols, num_sms,
+                                        static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fold gain");
+  return MOM_OK;
+}
+
+size_t mom_mlp_minseq_rmsnorm_workspace_bytes(int64_t S, int64_t hidden, int64_t intermediate, int64_t C,
+                                              mom_dtype_t dt) {
+  const size_t h = mom_mlp_minseq_workspace_bytes(S, hidden, intermediate, C, dt);
+  if (h == 0) return 0;
+  const int64_t rows = C < S ? C : S;
+  return h + ((static_cast<size_t>(rows) * 4 + 255) & ~static_cast<size_t>(255));
+}
+
+mom_status_t mom_mlp_minseq_rmsnorm_fwd(const void *x, const void *w_gate_folded, const void *w_up_folded,
+                                        const void *w_down, void *out, int64_t S, int64_t hidden,
+                                        int64_t intermediate, int64_t C, float eps, mom_dtype_t dt,
+                                        void *workspace, size_t workspace_bytes, mom_stream_t stream) {
+  g_err[0] = 0;
+  if (dt != MOM_BF16) return fail(MOM_ERR_UNSUPPORTED, "mom_mlp_minseq_rmsnorm_fwd: bf16 only");
+  if (!(eps >= 0.0f)) return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_rmsnorm_fwd: eps must be >= 0");
+  mom_status_t st = validate_minseq("mom_mlp_minseq_rmsnorm_fwd", x, x, w_gate_folded, w_up_folded, w_down, out, S,
+                                    hidden, intermediate, C, dt, workspace, workspace_bytes);
+  if (st != MOM_OK) return st;
+  const size_t need = mom_mlp_minseq_rmsnorm_workspace_bytes(S, hidden, intermediate, C, dt);
+  if (workspace_bytes < need)
+    return fail(MOM_ERR_WORKSPACE, "mom_mlp_minseq_rmsnorm_fwd: workspace %zu < required %zu bytes", workspace_bytes,
+                need);
+  return run_minseq(x, x, w_gate_folded, w_up_folded, w_down, out, S, hidden, intermediate, C, dt, workspace,
+                    static_cast<cudaStream_t>(stream), nullptr, nullptr, &eps);
 }
 
 size_t mom_mlp_last_token_workspace_bytes(int64_t intermediate) {

@@ -22,10 +22,17 @@ struct TcPhaseArgs {
   int cta_group;             // 1 or 2
   uint32_t group_m;          // raster group (0 = default)
   uint32_t policy;           // TMA L2 cache policy variant (0 = default)
+  const float *row_scale;    // phase A only: per-row scale of the gate/up accumulators (folded RMSNorm), or null
   int num_sms;
 };
 cudaError_t launch_phase_a_tc(const TcPhaseArgs &a, cudaStream_t stream);
 cudaError_t launch_phase_b_tc(const TcPhaseArgs &a, cudaStream_t stream);
+
+// folded RMSNorm (norm.cu)
+cudaError_t launch_fold_gain(const __nv_bfloat16 *w, const __nv_bfloat16 *g, __nv_bfloat16 *out, int64_t rows,
+                             int64_t cols, int num_sms, cudaStream_t stream);
+cudaError_t launch_row_inv_rms(const __nv_bfloat16 *x, float *r, int rows, int d, float eps, int num_sms,
+                               cudaStream_t stream);
 
 // fp32 SIMT path (mlp_simt.cu), row pointers already offset to the mini-sequence.
 cudaError_t launch_phase_a_f32(const float *x, const float *wg, const float *wu, float *h, int rows, int d, int I,

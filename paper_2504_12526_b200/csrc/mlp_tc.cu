@@ -70,6 +70,7 @@ struct Params {
   // epilogue
   __nv_bfloat16 *out;            // phase A: H_i [rows, I]; phase B: out rows [rows, d]
   const __nv_bfloat16 *residual; // phase B only, may be null
+  const float *row_scale;        // phase A only: folded-RMSNorm 1/rms per row, or null
   uint32_t ld_out;               // row pitch (elements) of out / residual
 };
 
@@ -225,12 +226,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t col0 = nt * TILE_N;
       if constexpr (PHASE_A) {
         __nv_bfloat16 *orow = p.out + static_cast<size_t>(row) * p.ld_out + col0;
+        // folded RMSNorm (f3): gate/up of row r are scaled by r's 1/rms before the SiLU
+        const float rs = (p.row_scale != nullptr && row_ok) ? p.row_scale[row] : 1.0f;
 #pragma unroll 1
         for (uint32_t c = 0; c < BHALF / 32; ++c) {
           uint32_t g[32], u[32];
           ptx::tmem_ld_32x32b_x32(taddr + c * 32, g);
           ptx::tmem_ld_32x32b_x32(taddr + BHALF + c * 32, u);
           ptx::tmem_ld_wait();
+          if (p.row_scale != nullptr) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              g[i] = __float_as_uint(__uint_as_float(g[i]) * rs);
+              u[i] = __float_as_uint(__uint_as_float(u[i]) * rs);
+            }
+          }
           uint32_t packed[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -352,6 +362,7 @@ cudaError_t launch_phase_a_tc(const TcPhaseArgs &a, cudaStream_t stream) {
   p.residual = nullptr;
   p.ld_out = a.ld_out;
   p.policy = a.policy;
+  p.row_scale = a.row_scale;
   if (a.cta_group == 2) return tc::launch<2, true>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
   return tc::launch<1, true>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
 }
@@ -369,6 +380,7 @@ cudaError_t launch_phase_b_tc(const TcPhaseArgs &a, cudaStream_t stream) {
   p.residual = a.residual;
   p.ld_out = a.ld_out;
   p.policy = a.policy;
+  p.row_scale = a.row_scale;
   if (a.cta_group == 2) return tc::launch<2, false>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
   return tc::launch<1, false>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
 }

@@ -257,3 +257,30 @@ def test_from_host_streamed_equals_device_input(cuda_device):
     assert torch.equal(out, ref)
     with pytest.raises(_mom.MomError):  # pageable host memory is rejected
         _mom.mlp_minseq_fwd_from_host(x.clone(), x_dev, x_dev, g[2], g[3], g[4], out, C, copy_stream=cp)
+
+
+# ------------------------------------------------------------------ f3: RMSNorm folded into phase A
+@pytest.mark.parametrize("S,d,I,C", [(1000, 512, 1024, 300), (4096, 4096, 14336, 2048)])
+def test_rmsnorm_folded_mlp(cuda_device, S, d, I, C):
+    """out = x + MLP(RMSNorm(x) * g) with g folded into W_gate/W_up and 1/rms applied to the
+    phase-A accumulators, against the oracle's literal norm-then-MLP."""
+    bf = torch.bfloat16
+    wg, wu, wd = synth.mlp_weights(d, I, 0, "cpu", bf)
+    gain = synth.norm_gain(d, "cpu", bf)
+    x = (synth.hidden(S, d, "cpu", torch.float32) * 3.0).to(bf)  # un-normed residual stream, rms ~ 3
+    eps = 1e-5
+    G = lambda t: t.to(cuda_device)  # noqa: E731
+    wg_f = _mom.fold_norm_gain(G(wg), G(gain))
+    wu_f = _mom.fold_norm_gain(G(wu), G(gain))
+    torch.cuda.synchronize()
+    assert torch.equal(wg_f.cpu(), (wg.float() * gain.float()).to(bf))  # RNE of w * g
+    out = torch.empty((S, d), dtype=bf, device=cuda_device)
+    _mom.mlp_minseq_rmsnorm_fwd(G(x), wg_f, wu_f, G(wd), out, C, eps)
+    torch.cuda.synchronize()
+    rows = synth.sample_rows(S, C, n_random=64) if S > 1000 else list(range(S))
+    ref = oracle.mlp_norm_rows(x, gain, eps, wg, wu, wd, rows)
+    check_close(out[rows].cpu(), ref, TOL_BF16, "folded RMSNorm MLP")
+    gx = G(x)
+    _mom.mlp_minseq_rmsnorm_fwd(gx, wg_f, wu_f, G(wd), gx, C, eps)  # in place
+    torch.cuda.synchronize()
+    assert torch.equal(gx, out)

@@ -274,3 +274,35 @@ def test_normwise_comparator():
     got = ref.copy(); got[1, 1] += 0.04
     assert abs(normwise_err(got, ref) - 0.01) < 1e-15
     assert normwise_err(np.array([np.nan]), np.array([1.0])) == float("inf")
+
+
+# ------------------------------------------------------------------ f3: norm folded into the MLP
+def test_norm_block_unit_rms_equals_plain_mlp():
+    """rows of +-1 have mean(x^2) = 1 exactly: with gain 1 and eps 0 RMSNorm is the identity, so the
+    block equals x + MLP(x) bitwise."""
+    S, d, I = 6, 16, 24
+    r = np.random.default_rng(90)
+    x = np.where(r.random((S, d)) < 0.5, -1.0, 1.0).astype(np.float32)
+    wg, wu, wd = rng_f32((I, d), 91, 0.3), rng_f32((I, d), 92, 0.3), rng_f32((d, I), 93, 0.2)
+    out = oracle.mlp_norm_rows(x, np.ones(d, np.float32), 0.0, wg, wu, wd, list(range(S)))
+    ref = oracle.mlp_rows(x, x, wg, wu, wd, list(range(S)))
+    assert out.tobytes() == ref.tobytes()
+
+
+def test_norm_block_closed_forms():
+    S, d, I = 5, 12, 20
+    x = rng_f32((S, d), 94, 3.0)
+    wg, wu, wd = rng_f32((I, d), 95, 0.3), rng_f32((I, d), 96, 0.3), rng_f32((d, I), 97, 0.2)
+    rows = list(range(S))
+    gain = (1 + 0.2 * rng_f32(d, 98)).astype(np.float32)
+    # gain 0 -> normed input 0 -> MLP(0) = 0 -> out = x exactly
+    assert np.array_equal(oracle.mlp_norm_rows(x, np.zeros(d, np.float32), 1e-6, wg, wu, wd, rows), x.astype(float))
+    # RMSNorm is scale invariant (eps = 0): the MLP part of 2x equals that of x
+    a = oracle.mlp_norm_rows(x, gain, 0.0, wg, wu, wd, rows) - x
+    b = oracle.mlp_norm_rows(2 * x, gain, 0.0, wg, wu, wd, rows) - 2 * x.astype(float)
+    assert np.max(np.abs(a - b)) <= 1e-13 * max(1.0, np.max(np.abs(a)))
+    # composition: rmsnorm() then the plain MLP on the (float32-rounded) normed rows
+    xn = np.stack([oracle.rmsnorm(x[i].astype(float), gain, 1e-5) for i in rows]).astype(np.float32)
+    ref = oracle.mlp_rows(xn, x, wg, wu, wd, rows)
+    got = oracle.mlp_norm_rows(x, gain, 1e-5, wg, wu, wd, rows)
+    assert np.max(np.abs(got - ref)) <= 1e-6 * np.max(np.abs(ref))
