@@ -169,6 +169,23 @@ mom_status_t mom_lm_head_last(const void *h_last, const void *norm_gain, float e
                               size_t workspace_bytes, mom_stream_t stream);
 
 /* ------------------------------------------------------------------------------------
+ * f2. Vocab-sharded LM head for token-sharded runs: rank r holds W_head rows
+ * [vocab_offset, vocab_offset + vocab_shard) and streams only those (1/N of the head's HBM
+ * bytes).  mom_lm_head_shard writes the shard's logits (optional) and *best_key, the u64
+ * (order-preserving fp32 value << 32 | (2^32-1 - global index)) of its best row; then
+ * mom_argmax_allreduce takes the u64 max over ranks (ncclAllReduce, ncclMax; comm == NULL
+ * for one rank) and decodes it, so every rank gets the global argmax with ties -> lowest
+ * index, bitwise equal to the unsharded mom_lm_head_last.
+ *   best_key: device uint64[1], 8-B aligned;  argmax: device int32[1].
+ * ---------------------------------------------------------------------------------- */
+mom_status_t mom_lm_head_shard(const void *h_last, const void *norm_gain, float eps,
+                               const void *w_head_shard, int64_t vocab_offset, int64_t vocab_shard,
+                               float *logits_shard, uint64_t *best_key, int64_t hidden,
+                               mom_dtype_t dt, void *workspace, size_t workspace_bytes,
+                               mom_stream_t stream);
+mom_status_t mom_argmax_allreduce(uint64_t *best_key, int32_t *argmax, void *comm, mom_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
  * a9. KV offload.  Alg. 1 P:99 "Update and offload KV cache to CPU"; sec. 3.2 P:127.
  * Records an event on producer_stream, makes copy_stream wait on it, enqueues one
  * cudaMemcpyAsync device->host of `bytes` on copy_stream, then records `done` on

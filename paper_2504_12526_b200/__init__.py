@@ -10,6 +10,8 @@ from ._mom import (  # noqa: F401
     LaunchTimer,
     MomError,
     allgather_rows,
+    argmax_allreduce,
+    lm_head_shard,
     kv_offload,
     kv_reload,
     lib,

@@ -34,6 +34,8 @@ SIGNATURES = {
     "mom_mlp_last_token": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _p, _sz, _p]),
     "mom_lm_head_workspace_bytes": (_sz, [_i64]),
     "mom_lm_head_last": (_i32, [_p, _p, _f32, _p, _p, _p, _i64, _i64, _i32, _p, _sz, _p]),
+    "mom_lm_head_shard": (_i32, [_p, _p, _f32, _p, _i64, _i64, _p, _p, _i64, _i32, _p, _sz, _p]),
+    "mom_argmax_allreduce": (_i32, [_p, _p, _p, _p]),
     "mom_kv_offload": (_i32, [_p, _p, _sz, _p, _p, _p]),
     "mom_kv_reload": (_i32, [_p, _p, _sz, _p, _p]),
     "mom_nccl_get_unique_id": (_i32, [_p]),
@@ -237,6 +239,25 @@ def lm_head_last(h_last, norm_gain, eps: float, w_head, logits, argmax, workspac
     _check(lib().mom_lm_head_last(_ptr(h_last), _ptr(norm_gain), float(eps), _ptr(w_head), _ptr(logits),
                                   _ptr(argmax), hidden, V, dt, _ptr(workspace),
                                   workspace.numel() * workspace.element_size(), _stream(stream)))
+    return argmax
+
+
+def lm_head_shard(h_last, norm_gain, eps: float, w_head_shard, vocab_offset: int, logits_shard, best_key,
+                  workspace=None, stream=None):
+    """f2: this rank's vocab shard of the LM head; best_key (device int64[1]) gets the packed best."""
+    hidden = h_last.shape[-1]
+    Vs = w_head_shard.shape[0]
+    if workspace is None:
+        workspace = torch.empty(lib().mom_lm_head_workspace_bytes(Vs), dtype=torch.uint8, device=h_last.device)
+    _check(lib().mom_lm_head_shard(_ptr(h_last), _ptr(norm_gain), float(eps), _ptr(w_head_shard), vocab_offset, Vs,
+                                   _ptr(logits_shard), _ptr(best_key), hidden, _dt(h_last), _ptr(workspace),
+                                   workspace.numel() * workspace.element_size(), _stream(stream)))
+    return best_key
+
+
+def argmax_allreduce(best_key, argmax, comm=None, stream=None):
+    """f2: u64 max of best_key over ranks (NCCL; comm None = one rank), decoded into argmax."""
+    _check(lib().mom_argmax_allreduce(_ptr(best_key), _ptr(argmax), comm, _stream(stream)))
     return argmax
 
 

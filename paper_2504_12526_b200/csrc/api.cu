@@ -470,10 +470,43 @@ mom_status_t mom_lm_head_last(const void *h_last, const void *norm_gain, float e
   if (num_sms > 256) num_sms = 256;
   cudaError_t e;
   ScopedTiming tm(static_cast<cudaStream_t>(stream), 5);
-  e = mom::launch_lm_head(h_last, norm_gain, eps, w_head, logits, argmax,
+  e = mom::launch_lm_head(h_last, norm_gain, eps, w_head, logits, argmax, nullptr, 0,
                                       static_cast<unsigned long long *>(workspace), (int)hidden, (int)vocab,
                                       dt == MOM_BF16, num_sms, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "lm head");
+  return MOM_OK;
+}
+
+mom_status_t mom_lm_head_shard(const void *h_last, const void *norm_gain, float eps, const void *w_head_shard,
+                               int64_t vocab_offset, int64_t vocab_shard, float *logits_shard, uint64_t *best_key,
+                               int64_t hidden, mom_dtype_t dt, void *workspace, size_t workspace_bytes,
+                               mom_stream_t stream) {
+  g_err[0] = 0;
+  if (!h_last || !w_head_shard || !best_key || !workspace)
+    return fail(MOM_ERR_INVALID_ARG, "mom_lm_head_shard: null pointer");
+  if (hidden < 1 || vocab_shard < 1 || vocab_offset < 0)
+    return fail(MOM_ERR_INVALID_ARG, "mom_lm_head_shard: bad sizes");
+  if (!valid_dtype(dt)) return fail(MOM_ERR_INVALID_ARG, "mom_lm_head_shard: bad dtype");
+  if (norm_gain && !(eps >= 0.0f)) return fail(MOM_ERR_INVALID_ARG, "mom_lm_head_shard: eps must be >= 0");
+  const size_t w = dtype_bytes(dt);
+  if ((hidden * w) % 16) return fail(MOM_ERR_INVALID_ARG, "mom_lm_head_shard: row pitch must be a multiple of 16 bytes");
+  if (!aligned16(h_last) || !aligned16(norm_gain) || !aligned16(w_head_shard) || !aligned16(logits_shard) ||
+      !aligned16(workspace) || (reinterpret_cast<uintptr_t>(best_key) & 7))
+    return fail(MOM_ERR_INVALID_ARG, "mom_lm_head_shard: misaligned pointer");
+  if (vocab_offset + vocab_shard > INT32_MAX - 1) return fail(MOM_ERR_INVALID_ARG, "mom_lm_head_shard: vocab exceeds int32");
+  if (static_cast<size_t>(hidden) * 4 > 200 * 1024)
+    return fail(MOM_ERR_UNSUPPORTED, "mom_lm_head_shard: hidden too large for shared-memory staging");
+  const size_t need = mom_lm_head_workspace_bytes(vocab_shard);
+  if (workspace_bytes < need) return fail(MOM_ERR_WORKSPACE, "mom_lm_head_shard: workspace %zu < %zu", workspace_bytes, need);
+  int num_sms = 0;
+  if (num_sms_current(&num_sms) != 0) return fail(MOM_ERR_CUDA, "mom_lm_head_shard: no CUDA device");
+  if (num_sms > 256) num_sms = 256;
+  ScopedTiming tm(static_cast<cudaStream_t>(stream), 5);
+  cudaError_t e = mom::launch_lm_head(h_last, norm_gain, eps, w_head_shard, logits_shard, nullptr,
+                                      reinterpret_cast<unsigned long long *>(best_key), (int)vocab_offset,
+                                      static_cast<unsigned long long *>(workspace), (int)hidden, (int)vocab_shard,
+                                      dt == MOM_BF16, num_sms, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "lm head shard");
   return MOM_OK;
 }
 
@@ -527,6 +560,7 @@ typedef int (*nccl_get_uid_fn)(nccl_uid_t *);
 typedef int (*nccl_init_fn)(void **, int, nccl_uid_t, int);
 typedef int (*nccl_destroy_fn)(void *);
 typedef int (*nccl_allgather_fn)(const void *, void *, size_t, int, void *, cudaStream_t);
+typedef int (*nccl_allreduce_fn)(const void *, void *, size_t, int, int, void *, cudaStream_t);
 typedef const char *(*nccl_errstr_fn)(int);
 struct Nccl {
   bool ok = false;
@@ -534,6 +568,7 @@ struct Nccl {
   nccl_init_fn init = nullptr;
   nccl_destroy_fn destroy = nullptr;
   nccl_allgather_fn allgather = nullptr;
+  nccl_allreduce_fn allreduce = nullptr;
   nccl_errstr_fn errstr = nullptr;
   char why[256] = "";
 };
@@ -551,8 +586,9 @@ Nccl &nccl() {
     n.init = reinterpret_cast<nccl_init_fn>(dlsym(h, "ncclCommInitRank"));
     n.destroy = reinterpret_cast<nccl_destroy_fn>(dlsym(h, "ncclCommDestroy"));
     n.allgather = reinterpret_cast<nccl_allgather_fn>(dlsym(h, "ncclAllGather"));
+    n.allreduce = reinterpret_cast<nccl_allreduce_fn>(dlsym(h, "ncclAllReduce"));
     n.errstr = reinterpret_cast<nccl_errstr_fn>(dlsym(h, "ncclGetErrorString"));
-    n.ok = n.get_uid && n.init && n.destroy && n.allgather;
+    n.ok = n.get_uid && n.init && n.destroy && n.allgather && n.allreduce;
     if (!n.ok) snprintf(n.why, sizeof(n.why), "libnccl.so.2 lacks a required symbol");
   });
   return n;
@@ -613,6 +649,24 @@ mom_status_t mom_allgather_rows(void *rows, int64_t rows_per_rank, int64_t hidde
   const void *send = static_cast<const char *>(rows) + static_cast<size_t>(rank) * count * w;  // in-place
   int rc = n.allgather(send, rows, count, nccl_dtype, comm, static_cast<cudaStream_t>(stream));
   if (rc != 0) return nccl_fail(rc, "ncclAllGather");
+  return MOM_OK;
+}
+
+mom_status_t mom_argmax_allreduce(uint64_t *best_key, int32_t *argmax, void *comm, mom_stream_t stream) {
+  g_err[0] = 0;
+  if (!best_key || !argmax) return fail(MOM_ERR_INVALID_ARG, "mom_argmax_allreduce: null pointer");
+  if ((reinterpret_cast<uintptr_t>(best_key) & 7) || (reinterpret_cast<uintptr_t>(argmax) & 3))
+    return fail(MOM_ERR_INVALID_ARG, "mom_argmax_allreduce: misaligned pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (comm) {
+    Nccl &n = nccl();
+    if (!n.ok) return fail(MOM_ERR_NCCL, "%s", n.why);
+    // u64 max over ranks of (order-preserving value << 32 | ~index): max logit, lowest index on ties
+    int rc = n.allreduce(best_key, best_key, 1, 5 /* ncclUint64 */, 2 /* ncclMax */, comm, s);
+    if (rc != 0) return nccl_fail(rc, "ncclAllReduce(max)");
+  }
+  cudaError_t e = mom::launch_key_to_index(reinterpret_cast<const unsigned long long *>(best_key), argmax, s);
+  if (e != cudaSuccess) return cuda_fail(e, "key to index");
   return MOM_OK;
 }
 

@@ -154,7 +154,8 @@ template <bool BF16>
 __global__ void __launch_bounds__(THREADS) lm_head_gemv(const void *__restrict__ hin, const void *__restrict__ gain,
                                                         float eps, const void *__restrict__ w,
                                                         float *__restrict__ logits,
-                                                        unsigned long long *__restrict__ partials, int d, int V) {
+                                                        unsigned long long *__restrict__ partials, int d, int V,
+                                                        int vocab_offset) {
   extern __shared__ float hs[];
   __shared__ float red[WARPS];
   __shared__ unsigned long long best_s[WARPS];
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(THREADS) lm_head_gemv(const void *__restrict__
     const float s = row_dot<BF16>(static_cast<const char *>(w) + v * pitch, hs, d, lane);
     if (lane == 0) {
       if (logits) logits[v] = s;
-      const unsigned long long key = pack_key(s, v);
+      const unsigned long long key = pack_key(s, v + vocab_offset);  // global vocab index
       best = key > best ? key : best;
     }
   }
@@ -197,7 +198,10 @@ __global__ void __launch_bounds__(THREADS) lm_head_gemv(const void *__restrict__
   }
 }
 
-__global__ void argmax_reduce(const unsigned long long *__restrict__ partials, int n, int32_t *__restrict__ out) {
+// Max over the per-block keys; writes the argmax (ties -> lowest index) and/or the packed key
+// (the latter feeds the cross-rank u64 max of the vocab-sharded head, f2).
+__global__ void argmax_reduce(const unsigned long long *__restrict__ partials, int n, int32_t *__restrict__ out,
+                              unsigned long long *__restrict__ key_out) {
   __shared__ unsigned long long s[32];
   unsigned long long b = 0ull;
   for (int i = threadIdx.x; i < n; i += blockDim.x) b = partials[i] > b ? partials[i] : b;
@@ -207,8 +211,15 @@ __global__ void argmax_reduce(const unsigned long long *__restrict__ partials, i
   if (threadIdx.x < 32) {
     b = threadIdx.x < blockDim.x / 32 ? s[threadIdx.x] : 0ull;
     b = warp_max_u64(b);
-    if (threadIdx.x == 0) out[0] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(b & 0xFFFFFFFFull));
+    if (threadIdx.x == 0) {
+      if (out) out[0] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(b & 0xFFFFFFFFull));
+      if (key_out) key_out[0] = b;
+    }
   }
+}
+
+__global__ void key_to_index(const unsigned long long *__restrict__ key, int32_t *__restrict__ out) {
+  out[0] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(key[0] & 0xFFFFFFFFull));
 }
 
 template <typename K>
@@ -248,7 +259,8 @@ cudaError_t launch_last_token_mlp(const void *x, const void *residual, const voi
 size_t lm_head_partials(int num_sms) { return static_cast<size_t>(num_sms) * 4; }
 
 cudaError_t launch_lm_head(const void *h, const void *gain, float eps, const void *w, float *logits,
-                           int32_t *argmax, unsigned long long *partials, int d, int V, bool is_bf16, int num_sms,
+                           int32_t *argmax, unsigned long long *key_out, int vocab_offset,
+                           unsigned long long *partials, int d, int V, bool is_bf16, int num_sms,
                            cudaStream_t stream) {
   using namespace gemv;
   const size_t smem = static_cast<size_t>(d) * sizeof(float);
@@ -258,12 +270,17 @@ cudaError_t launch_lm_head(const void *h, const void *gain, float eps, const voi
   cudaError_t e;
   if (is_bf16) {
     if ((e = set_smem(lm_head_gemv<true>, smem)) != cudaSuccess) return e;
-    lm_head_gemv<true><<<blocks, THREADS, smem, stream>>>(h, gain, eps, w, logits, partials, d, V);
+    lm_head_gemv<true><<<blocks, THREADS, smem, stream>>>(h, gain, eps, w, logits, partials, d, V, vocab_offset);
   } else {
     if ((e = set_smem(lm_head_gemv<false>, smem)) != cudaSuccess) return e;
-    lm_head_gemv<false><<<blocks, THREADS, smem, stream>>>(h, gain, eps, w, logits, partials, d, V);
+    lm_head_gemv<false><<<blocks, THREADS, smem, stream>>>(h, gain, eps, w, logits, partials, d, V, vocab_offset);
   }
-  argmax_reduce<<<1, 1024, 0, stream>>>(partials, blocks, argmax);
+  argmax_reduce<<<1, 1024, 0, stream>>>(partials, blocks, argmax, key_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_key_to_index(const unsigned long long *key, int32_t *argmax, cudaStream_t stream) {
+  gemv::key_to_index<<<1, 1, 0, stream>>>(key, argmax);
   return cudaGetLastError();
 }
 

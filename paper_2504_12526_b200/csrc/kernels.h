@@ -46,7 +46,9 @@ cudaError_t launch_last_token_mlp(const void *x, const void *residual, const voi
                                   int num_sms, cudaStream_t stream);
 size_t lm_head_partials(int num_sms);
 cudaError_t launch_lm_head(const void *h, const void *gain, float eps, const void *w, float *logits,
-                           int32_t *argmax, unsigned long long *partials, int d, int V, bool is_bf16, int num_sms,
+                           int32_t *argmax, unsigned long long *key_out, int vocab_offset,
+                           unsigned long long *partials, int d, int V, bool is_bf16, int num_sms,
                            cudaStream_t stream);
+cudaError_t launch_key_to_index(const unsigned long long *key, int32_t *argmax, cudaStream_t stream);
 
 }  // namespace mom

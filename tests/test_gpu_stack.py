@@ -106,3 +106,54 @@ def test_nccl_allgather_single_rank(cuda_device):
     torch.cuda.synchronize()
     _mom.nccl_comm_destroy(comm)
     assert torch.equal(rows, ref)
+
+
+@pytest.mark.parametrize("nshards", [2, 3, 8])
+def test_vocab_sharded_lm_head(cuda_device, nshards):
+    """f2: the vocab-sharded head (each shard streams V/N rows of W_head and emits a packed u64
+    best key; the u64 max over shards is the argmax) equals the unsharded head bitwise:
+    logits concatenate to the unsharded logits and the combined key decodes to its argmax."""
+    import numpy as np
+    w = synth.CONFIGS[1]
+    d, V = w.hidden, w.vocab
+    bf = torch.bfloat16
+    wh = synth.head_weight(V, d, cuda_device, bf)
+    gain = synth.norm_gain(d, cuda_device, bf)
+    y = synth.hidden(1, d, cuda_device, bf)[0]
+    logits = torch.empty(V, dtype=torch.float32, device=cuda_device)
+    am = torch.empty(1, dtype=torch.int32, device=cuda_device)
+    _mom.lm_head_last(y, gain, w.eps, wh, logits, am)
+    shard_logits = torch.empty(V, dtype=torch.float32, device=cuda_device)
+    keys = torch.zeros(nshards, dtype=torch.int64, device=cuda_device)
+    per = -(-V // nshards)
+    for r in range(nshards):
+        v0, v1 = r * per, min(V, (r + 1) * per)
+        _mom.lm_head_shard(y, gain, w.eps, wh[v0:v1], v0, shard_logits[v0:v1], keys[r:r + 1])
+    torch.cuda.synchronize()
+    assert torch.equal(shard_logits, logits)
+    k = keys.cpu().numpy().view(np.uint64)
+    best = int(k.max())
+    assert 0xFFFFFFFF - (best & 0xFFFFFFFF) == int(am.item())
+    win = torch.tensor([int(k.argmax())], device=cuda_device)
+    am2 = torch.empty(1, dtype=torch.int32, device=cuda_device)
+    _mom.argmax_allreduce(keys[win.item():win.item() + 1], am2, None)  # decode only (one rank)
+    torch.cuda.synchronize()
+    assert int(am2.item()) == int(am.item()) == oracle.argmax_f32(logits.cpu().numpy())
+
+
+def test_argmax_allreduce_nccl_single_rank(cuda_device):
+    d, V = 512, 5000
+    bf = torch.bfloat16
+    wh = synth.head_weight(V, d, cuda_device, bf)
+    y = synth.hidden(1, d, cuda_device, bf)[0]
+    key = torch.zeros(1, dtype=torch.int64, device=cuda_device)
+    _mom.lm_head_shard(y, None, 0.0, wh, 0, None, key)
+    uid = _mom.nccl_get_unique_id()
+    comm = _mom.nccl_comm_init(1, uid, 0)
+    am = torch.empty(1, dtype=torch.int32, device=cuda_device)
+    _mom.argmax_allreduce(key, am, comm)
+    ref = torch.empty(1, dtype=torch.int32, device=cuda_device)
+    _mom.lm_head_last(y, None, 0.0, wh, None, ref)
+    torch.cuda.synchronize()
+    _mom.nccl_comm_destroy(comm)
+    assert int(am.item()) == int(ref.item())
