@@ -293,31 +293,45 @@ def run_mine(args):
     ms = max_over_ranks(ms_local, world, device)
     total_tokens = world * wl.S
     value = total_tokens / (ms / 1e3)
-    n_launch = int(sum_over_ranks(launches[0], world, device))
+    # kernels of ours launched in the timed region (the GEMV entries launch 2 kernels each)
+    n_local = sum(2 if k in ("last_token_gemv", "lm_head_gemv") else 1 for k, _ in timer.results())
+    n_launch = int(sum_over_ranks(n_local, world, device))
 
     # per-kernel times (live, same timed region)
     per = {}
     for kind, t in timer.results():
         per.setdefault(kind, []).append(t)
     d, I, C, S = wl.d, wl.I, wl.C, wl.S
-    flops_a = 4.0 * C * d * I      # gate + up projections of one mini-sequence (2 GEMMs, 2 flop/MAC)
-    flops_b = 2.0 * C * d * I      # down projection
-    ta = statistics.mean(per["phaseA_tc"]) if "phaseA_tc" in per else float("nan")
-    tb = statistics.mean(per["phaseB_tc"]) if "phaseB_tc" in per else float("nan")
     sustained = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
     burst = peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"])
     hbm = peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
-    ach_a = flops_a / (ta * 1e-3) / 1e12
-    ach_b = flops_b / (tb * 1e-3) / 1e12
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "phaseA_dram_bytes.json")
+    if "mlp_fused_tc" in per:
+        # both phases of one mini-sequence in one persistent launch: 6*C*d*I FLOP per launch
+        dom_name = "mlp_fused_tc (gate/up GEMM + SiLU*mul and down GEMM + residual, one tcgen05 launch)"
+        flops_dom = 6.0 * C * d * I
+        t_dom = statistics.mean(per["mlp_fused_tc"])
+        tpath = os.path.join(ROOT, "profiles", "fused_dram_bytes.json")
+        mlp_ms = wl.M * t_dom
+    else:
+        dom_name = "phaseA_tc (gate/up GEMM + SiLU*mul, tcgen05)"
+        flops_dom = 4.0 * C * d * I   # gate + up projections of one mini-sequence (2 GEMMs, 2 flop/MAC)
+        t_dom = statistics.mean(per["phaseA_tc"])
+        tpath = os.path.join(ROOT, "profiles", "phaseA_dram_bytes.json")
+        mlp_ms = wl.M * (t_dom + statistics.mean(per["phaseB_tc"]))
     if os.path.exists(tpath):
         try:
             traffic = json.load(open(tpath)).get("bytes_per_launch")
         except Exception:
             traffic = None
-    kernels = {"phaseA_tc": {"ms": ta, "tflops": ach_a, "frac_sustained": ach_a / sustained},
-               "phaseB_tc": {"ms": tb, "tflops": ach_b, "frac_sustained": ach_b / sustained}}
+    ach_a = flops_dom / (t_dom * 1e-3) / 1e12
+    flops_a = flops_dom
+    kernels = {}
+    for name, fl in (("mlp_fused_tc", 6.0), ("phaseA_tc", 4.0), ("phaseB_tc", 2.0)):
+        if name in per:
+            t = statistics.mean(per[name])
+            tf = fl * C * d * I / (t * 1e-3) / 1e12
+            kernels[name] = {"ms": t, "tflops": tf, "frac_burst": tf / burst, "frac_sustained": tf / sustained}
     if "last_token_gemv" in per:
         t = statistics.mean(per["last_token_gemv"])
         gbs = 3.0 * d * I * 2 / (t * 1e-3) / 1e9
@@ -326,8 +340,6 @@ def run_mine(args):
         t = statistics.mean(per["lm_head_gemv"])
         gbs = 1.0 * wl.V * d * 2 / (t * 1e-3) / 1e9
         kernels["lm_head_gemv"] = {"ms": t, "gbs": gbs, "frac_hbm": gbs / hbm}
-    mlp_ms = wl.M * (ta + tb)
-
     result = {
         "metric": "prefill MLP tokens/s (MOM mini-sequence path: KV offload + M-chunk SwiGLU MLP + last-token MLP/LM head/argmax + KV reload)",
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -337,10 +349,12 @@ def run_mine(args):
                    "seq_len_per_gpu": S, "global_tokens": total_tokens, "minseq_len": C, "M": wl.M,
                    "kv_bytes_per_layer": wl.kv.numel() * 2, "parallelism": f"token-shard x{world}",
                    "l2": "inputs larger than L2 (x 537 MB, weights 352 MB/layer, W_head 1.05 GB)"},
-        "roofline": {"kernel": "phaseA_tc (gate/up GEMM + SiLU*mul, tcgen05)", "bound": "tensor",
-                     "achieved": ach_a, "peak": sustained, "unit": "TFLOP/s", "frac": ach_a / sustained,
-                     "traffic": traffic, "peak_source": peaks_src + " bf16_tflops_sustained (kernel timed inside a long step)",
-                     "frac_of_burst_peak": ach_a / burst, "flop_per_launch": flops_a},
+        "roofline": {"kernel": dom_name, "bound": "tensor",
+                     "achieved": ach_a, "peak": burst, "unit": "TFLOP/s", "frac": ach_a / burst,
+                     "traffic": traffic,
+                     "peak_source": peaks_src + " bf16_tflops (burst; the conservative choice: the timed region is "
+                                    "well under the 4 s of the sustained measurement)",
+                     "frac_of_sustained_peak": ach_a / sustained, "flop_per_launch": flops_a},
         "kernels": kernels,
         "mlp_only": {"ms": mlp_ms, "tokens_per_s": S / (mlp_ms * 1e-3),
                      "tflops": 6.0 * S * d * I / (mlp_ms * 1e-3) / 1e12,

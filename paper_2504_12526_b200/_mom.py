@@ -46,7 +46,8 @@ SIGNATURES = {
 }
 
 KIND_NAMES = {0: "phaseA_tc", 1: "phaseB_tc", 2: "phaseA_f32", 3: "phaseB_f32", 4: "last_token_gemv",
-              5: "lm_head_gemv"}
+              5: "lm_head_gemv", 6: "mlp_fused_tc"}
+KERNELS_PER_KIND = {4: 2, 5: 2}  # the GEMV kinds launch two kernels each (plus 1 for the others)
 
 
 class LaunchTimer:

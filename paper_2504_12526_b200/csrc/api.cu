@@ -134,6 +134,13 @@ mom_status_t check_pinned(const void *host, const char *who) {
   return MOM_OK;
 }
 
+// bytes of one mini-sequence's intermediate H_i = min(C, S) * I * w, rounded to 256 B
+size_t h_bytes(int64_t S, int64_t I, int64_t C, mom_dtype_t dt) {
+  const int64_t rows = C < S ? C : S;
+  const size_t b = static_cast<size_t>(rows) * static_cast<size_t>(I) * dtype_bytes(dt);
+  return (b + 255) & ~static_cast<size_t>(255);
+}
+
 int env_int(const char *name, int dflt) {
   const char *v = getenv(name);
   return (v && *v) ? atoi(v) : dflt;
@@ -179,9 +186,10 @@ size_t mom_mlp_minseq_workspace_bytes(int64_t S, int64_t hidden, int64_t interme
                                       mom_dtype_t dt) {
   (void)hidden;
   if (S < 1 || intermediate < 1 || C < 1 || !valid_dtype(dt)) return 0;
-  const int64_t rows = C < S ? C : S;  // one mini-sequence's H_i: C * I elements (Eq. 3)
-  const size_t b = static_cast<size_t>(rows) * static_cast<size_t>(intermediate) * dtype_bytes(dt);
-  return (b + 255) & ~static_cast<size_t>(255);
+  const size_t h = h_bytes(S, intermediate, C, dt);  // one mini-sequence's H_i: C * I elements (Eq. 3)
+  if (dt == MOM_F32) return h;
+  const int64_t rows = C < S ? C : S;  // + the fused kernel's per-row-block counters (<= ~4 KB at C = 8192)
+  return h + ((mom::mlp_tc_ready_counters(static_cast<uint32_t>(rows)) * 4 + 255) & ~static_cast<size_t>(255));
 }
 
 }  // extern "C"
@@ -228,6 +236,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
   const uint32_t group_a = static_cast<uint32_t>(env_int("MOM_GROUP_M_A", 0));
   const uint32_t group_b = static_cast<uint32_t>(env_int("MOM_GROUP_M_B", 0));
   const uint32_t policy = static_cast<uint32_t>(env_int("MOM_TMA_POLICY", 0));
+  const bool fused = env_int("MOM_FUSED", 1) != 0;
   CUtensorMap tm_wg, tm_wu, tm_wd;
   mom_status_t st;
   if (dt == MOM_BF16) {
@@ -279,13 +288,14 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     CUtensorMap tm_x, tm_h;
     if ((st = make_tmap(&tm_x, xi, rows, hidden, "x_i")) != MOM_OK) return st;
     if ((st = make_tmap(&tm_h, h, rows, intermediate, "h_i")) != MOM_OK) return st;
-    mom::TcPhaseArgs a{};
-    a.tm_a = &tm_x; a.tm_b0 = &tm_wg; a.tm_b1 = &tm_wu;
-    a.rows = (uint32_t)rows; a.n_out = (uint32_t)intermediate; a.k = (uint32_t)hidden;
-    a.out = h; a.residual = nullptr; a.ld_out = (uint32_t)intermediate;
-    a.cta_group = cta_group; a.group_m = group_a; a.policy = policy; a.num_sms = num_sms;
+    mom::TcMlpArgs a{};
+    a.tm_x = &tm_x; a.tm_wg = &tm_wg; a.tm_wu = &tm_wu; a.tm_h = &tm_h; a.tm_wd = &tm_wd;
+    a.rows = (uint32_t)rows; a.d = (uint32_t)hidden; a.I = (uint32_t)intermediate;
+    a.h = h; a.out = static_cast<__nv_bfloat16 *>(oi); a.residual = static_cast<const __nv_bfloat16 *>(ri);
+    a.cta_group = cta_group; a.policy = policy; a.num_sms = num_sms;
+    a.ready = reinterpret_cast<uint32_t *>(static_cast<char *>(workspace) + h_bytes(S, intermediate, C, dt));
     if (norm_eps) {
-      // folded RMSNorm (f3): 1/rms of this mini-sequence's rows, after H_i in the workspace
+      // folded RMSNorm (f3): 1/rms of this mini-sequence's rows, after H_i and the counters
       float *inv = reinterpret_cast<float *>(static_cast<char *>(workspace) +
                                              mom_mlp_minseq_workspace_bytes(S, hidden, intermediate, C, dt));
       e = mom::launch_row_inv_rms(static_cast<const __nv_bfloat16 *>(xi), inv, (int)rows, (int)hidden, *norm_eps,
@@ -293,20 +303,27 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
       if (e != cudaSuccess) return cuda_fail(e, "row 1/rms");
       a.row_scale = inv;
     }
+    if (fused) {
+      // one persistent launch: H_i = Swish(A_i Wg^T) (.) A_i Wu^T and O_i = R_i + H_i Wd^T,
+      // O_i written at rows r0..; phase-B tiles wait on per-row-block counters
+      e = cudaMemsetAsync(a.ready, 0, mom::mlp_tc_ready_counters((uint32_t)rows) * sizeof(uint32_t), stream);
+      if (e != cudaSuccess) return cuda_fail(e, "counter reset");
+      a.group_m = group_a;
+      ScopedTiming tm(stream, 6);
+      e = mom::launch_mlp_tc(a, 2, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "fused MLP (tcgen05)");
+      continue;
+    }
+    a.group_m = group_a;
     {
       ScopedTiming tm(stream, 0);
-      e = mom::launch_phase_a_tc(a, stream);  // H_i = Swish(A_i Wg^T) (.) A_i Wu^T
+      e = mom::launch_mlp_tc(a, 0, stream);  // H_i = Swish(A_i Wg^T) (.) A_i Wu^T
     }
     if (e != cudaSuccess) return cuda_fail(e, "phase A (tcgen05)");
-    mom::TcPhaseArgs b{};
-    b.tm_a = &tm_h; b.tm_b0 = &tm_wd; b.tm_b1 = &tm_wd;
-    b.rows = (uint32_t)rows; b.n_out = (uint32_t)hidden; b.k = (uint32_t)intermediate;
-    b.out = static_cast<__nv_bfloat16 *>(oi); b.residual = static_cast<const __nv_bfloat16 *>(ri);
-    b.ld_out = (uint32_t)hidden;
-    b.cta_group = cta_group; b.group_m = group_b; b.policy = policy; b.num_sms = num_sms;
+    a.group_m = group_b;
     {
       ScopedTiming tm(stream, 1);
-      e = mom::launch_phase_b_tc(b, stream);  // O_i = R_i + H_i Wd^T, written at rows r0..
+      e = mom::launch_mlp_tc(a, 1, stream);  // O_i = R_i + H_i Wd^T, written at rows r0..
     }
     if (e != cudaSuccess) return cuda_fail(e, "phase B (tcgen05)");
   }

@@ -8,25 +8,28 @@
 
 namespace mom {
 
-// One phase of one mini-sequence on the tcgen05 path (mlp_tc.cu).
-struct TcPhaseArgs {
-  const CUtensorMap *tm_a;   // A operand rows (X_i for phase A, H_i for phase B), box 64 x 128
-  const CUtensorMap *tm_b0;  // phase A: W_gate; phase B: W_down
-  const CUtensorMap *tm_b1;  // phase A: W_up;   phase B: W_down (second 128-row half)
+// One mini-sequence on the tcgen05 path (mlp_tc.cu).  Tensor maps are 2D bf16, box 64 x 128.
+struct TcMlpArgs {
+  const CUtensorMap *tm_x;   // X_i [C_i, d]    (phase A operand A)
+  const CUtensorMap *tm_wg;  // W_gate [I, d]   (phase A B half 0)
+  const CUtensorMap *tm_wu;  // W_up [I, d]     (phase A B half 1)
+  const CUtensorMap *tm_h;   // H_i [C_i, I]    (phase B operand A)
+  const CUtensorMap *tm_wd;  // W_down [d, I]   (phase B B halves)
   uint32_t rows;             // C_i
-  uint32_t n_out;            // I (phase A) or hidden (phase B)
-  uint32_t k;                // hidden (phase A) or I (phase B)
-  __nv_bfloat16 *out;        // H_i or out rows
-  const __nv_bfloat16 *residual;  // phase B, may be null
-  uint32_t ld_out;           // row pitch of out/residual in elements
+  uint32_t d, I;
+  __nv_bfloat16 *h;          // H_i (workspace)
+  __nv_bfloat16 *out;        // out rows of this mini-sequence
+  const __nv_bfloat16 *residual;  // may be null
+  const float *row_scale;    // folded RMSNorm 1/rms per row (phase A), or null
+  uint32_t *ready;           // fused mode: mlp_tc_ready_counters(rows) zeroed counters
   int cta_group;             // 1 or 2
   uint32_t group_m;          // raster group (0 = default)
   uint32_t policy;           // TMA L2 cache policy variant (0 = default)
-  const float *row_scale;    // phase A only: per-row scale of the gate/up accumulators (folded RMSNorm), or null
   int num_sms;
 };
-cudaError_t launch_phase_a_tc(const TcPhaseArgs &a, cudaStream_t stream);
-cudaError_t launch_phase_b_tc(const TcPhaseArgs &a, cudaStream_t stream);
+// mode 0: phase A only, 1: phase B only, 2: both phases in one persistent launch.
+cudaError_t launch_mlp_tc(const TcMlpArgs &a, int mode, cudaStream_t stream);
+size_t mlp_tc_ready_counters(uint32_t rows);
 
 // folded RMSNorm (norm.cu)
 cudaError_t launch_fold_gain(const __nv_bfloat16 *w, const __nv_bfloat16 *g, __nv_bfloat16 *out, int64_t rows,

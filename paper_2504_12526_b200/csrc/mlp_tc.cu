@@ -1,7 +1,7 @@
 // mlp_tc.cu -- tcgen05/TMEM/TMA kernels for the bf16 mini-sequence SwiGLU MLP
 // (Alg. 1 P:109-113 of arXiv 2504.12526; MLP = SwiGLU).
 //
-// One persistent, warp-specialised "dual-B" GEMM serves both phases of a mini-sequence:
+// One persistent, warp-specialised "dual-B" GEMM kernel computes both phases of a mini-sequence:
 //
 //   Phase A  (gate/up + SiLU*mul):  acc[:, 0:128]   = X_i Wg[n0:n0+128]^T
 //                                   acc[:, 128:256] = X_i Wu[n0:n0+128]^T
@@ -11,6 +11,15 @@
 //
 // so one UMMA with N = 256 computes the gate and up tiles of the same 128 intermediate
 // columns side by side in TMEM, and the [S, I] gate/up tensors never exist (Eq. 1).
+//
+// MODE_A / MODE_B run one phase per launch.  MODE_FUSED runs the whole mini-sequence in ONE
+// persistent launch: tiles are ordered by groups of `group_m` 256-row blocks, each group's
+// phase-A tiles followed by its phase-B tiles, and a phase-B tile's producer waits (acquire
+// spin on a per-row-block counter that phase-A epilogues release) until all phase-A tiles of
+// its row block have written H.  Phase B of group g thus overlaps phase A of group g+1: no
+// launch gap and no wave-quantisation tail between the phases, and H rows are re-read soon
+// after they were written.  Deadlock-free: a tile only waits on tiles with smaller indices,
+// every CTA walks its tiles in increasing order, and the grid is co-resident (persistent).
 //
 // Roles (256 threads): warp 0 = TMA producer (1 lane), warp 1 = TMEM allocator + MMA issuer
 // (1 lane), warps 4..7 = epilogue (TMEM lane quarter q = warp - 4, one row per thread).
@@ -22,17 +31,17 @@
 //         A rows [128r, 128r+128) and B half r; the leader CTA issues the MMAs; both CTAs
 //         hold their 128 rows x 256 columns of the accumulator in their own TMEM.
 //
-// Determinism: no split-K, no atomics, the tile shape does not depend on the mini-sequence
-// length, and every accumulator sums K in the same order -> outputs are bitwise identical
-// for every mini-sequence count M (the paper's "identical logits").
+// Determinism: no split-K, no atomics on data, the tile shape does not depend on the
+// mini-sequence length, and every accumulator sums K in the same order -> outputs are bitwise
+// identical for every mini-sequence count M and for fused vs unfused ("identical logits").
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
-#include "ptx.cuh"
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace mom {
 
@@ -49,6 +58,8 @@ constexpr uint32_t ACC_COLS = 256;
 constexpr uint32_t NUM_THREADS = 256;
 constexpr uint32_t EPI_WARP0 = 4;
 
+enum : int { MODE_A = 0, MODE_B = 1, MODE_FUSED = 2 };
+
 template <int CG>
 struct Cfg {
   static constexpr uint32_t B_BYTES = (CG == 1 ? 2 : 1) * BHALF_BYTES;  // B bytes staged per CTA
@@ -58,31 +69,67 @@ struct Cfg {
   static constexpr uint32_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
 };
 
-struct Params {
-  // problem
-  uint32_t rows;         // valid rows of this mini-sequence (C_i)
-  uint32_t n_out;        // output columns (I for phase A, d for phase B)
-  uint32_t k;            // reduction length (d for phase A, I for phase B)
-  uint32_t m_tiles;      // ceil(rows / (BM*CG))
-  uint32_t n_tiles;      // ceil(n_out / tile_n)
-  uint32_t group_m;      // raster: M tiles per group (N iterates inside a group)
-  uint32_t policy;       // TMA L2 policy: 0 reuse-aware (default), 1 all evict_normal, 2 A evict_first
-  // epilogue
-  __nv_bfloat16 *out;            // phase A: H_i [rows, I]; phase B: out rows [rows, d]
-  const __nv_bfloat16 *residual; // phase B only, may be null
-  const float *row_scale;        // phase A only: folded-RMSNorm 1/rms per row, or null
-  uint32_t ld_out;               // row pitch (elements) of out / residual
+// The five operands of one mini-sequence (unused ones are copies in single-phase modes).
+struct Maps {
+  CUtensorMap x;   // A of phase A: X_i [C_i, d]
+  CUtensorMap wg;  // B half 0 of phase A: W_gate [I, d]
+  CUtensorMap wu;  // B half 1 of phase A: W_up [I, d]
+  CUtensorMap h;   // A of phase B: H_i [C_i, I]
+  CUtensorMap wd;  // B halves of phase B: W_down [d, I]
 };
 
-__device__ __forceinline__ void tile_coords(uint32_t t, const Params &p, uint32_t &m, uint32_t &n) {
-  const uint32_t per_group = p.group_m * p.n_tiles;
-  const uint32_t g = t / per_group;
-  const uint32_t local = t - g * per_group;
-  const uint32_t m0 = g * p.group_m;
-  uint32_t gm = p.m_tiles - m0;
-  if (gm > p.group_m) gm = p.group_m;
-  m = m0 + local % gm;
-  n = local / gm;
+struct Params {
+  uint32_t rows;         // valid rows of this mini-sequence (C_i)
+  uint32_t d, I;         // hidden, intermediate
+  uint32_t m_tiles;      // ceil(rows / (BM*CG))
+  uint32_t nA, nB;       // N tiles of phase A (I/128) and phase B (d/256)
+  uint32_t group_m;      // raster: row blocks per group (N iterates inside a group)
+  uint32_t policy;       // TMA L2 policy: 0 reuse-aware (default), 1 all evict_normal, 2 A evict_first
+  __nv_bfloat16 *h;              // phase A output H_i [rows, I]
+  __nv_bfloat16 *out;            // phase B output rows [rows, d]
+  const __nv_bfloat16 *residual; // phase B residual, may be null
+  const float *row_scale;        // phase A: folded-RMSNorm 1/rms per row, or null
+  uint32_t *ready;               // MODE_FUSED: per (row block, CTA rank) count of finished phase-A tiles
+};
+
+struct Tile {
+  uint32_t m, n;
+  bool a;  // phase A tile
+};
+
+template <int MODE>
+__device__ __forceinline__ Tile decode_tile(uint32_t t, const Params &p) {
+  Tile tl;
+  const uint32_t G = p.group_m;
+  if constexpr (MODE == MODE_FUSED) {
+    const uint32_t per_group = G * (p.nA + p.nB);
+    const uint32_t g = t / per_group;
+    uint32_t local = t - g * per_group;
+    const uint32_t m0 = g * G;
+    uint32_t gm = p.m_tiles - m0;
+    if (gm > G) gm = G;
+    tl.a = local < gm * p.nA;
+    if (!tl.a) local -= gm * p.nA;
+    tl.m = m0 + local % gm;
+    tl.n = local / gm;
+  } else {
+    const uint32_t nt = MODE == MODE_A ? p.nA : p.nB;
+    const uint32_t per_group = G * nt;
+    const uint32_t g = t / per_group;
+    const uint32_t local = t - g * per_group;
+    const uint32_t m0 = g * G;
+    uint32_t gm = p.m_tiles - m0;
+    if (gm > G) gm = G;
+    tl.m = m0 + local % gm;
+    tl.n = local / gm;
+    tl.a = MODE == MODE_A;
+  }
+  return tl;
+}
+
+template <int MODE>
+__host__ __device__ __forceinline__ uint32_t num_tiles_of(const Params &p) {
+  return MODE == MODE_A ? p.m_tiles * p.nA : MODE == MODE_B ? p.m_tiles * p.nB : p.m_tiles * (p.nA + p.nB);
 }
 
 __device__ __forceinline__ float silu_mul(float g, float u) {
@@ -90,10 +137,92 @@ __device__ __forceinline__ float silu_mul(float g, float u) {
   return g / (1.0f + __expf(-g)) * u;
 }
 
-template <int CG, bool PHASE_A>
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Phase A epilogue for one tile: H[row, col0 + j] = bf16(silu(g_j * rs) * (u_j * rs)), j < 128.
+__device__ __forceinline__ void epilogue_a(const Params &p, uint32_t taddr, uint32_t row, bool row_ok, uint32_t col0) {
+  __nv_bfloat16 *orow = p.h + static_cast<size_t>(row) * p.I + col0;
+  // folded RMSNorm (f3): gate/up of row r are scaled by r's 1/rms before the SiLU
+  const float rs = (p.row_scale != nullptr && row_ok) ? p.row_scale[row] : 1.0f;
+#pragma unroll 1
+  for (uint32_t c = 0; c < BHALF / 32; ++c) {
+    uint32_t g[32], u[32];
+    ptx::tmem_ld_32x32b_x32(taddr + c * 32, g);
+    ptx::tmem_ld_32x32b_x32(taddr + BHALF + c * 32, u);
+    ptx::tmem_ld_wait();
+    if (p.row_scale != nullptr) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        g[i] = __float_as_uint(__uint_as_float(g[i]) * rs);
+        u[i] = __float_as_uint(__uint_as_float(u[i]) * rs);
+      }
+    }
+    uint32_t packed[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float h0 = silu_mul(__uint_as_float(g[2 * i]), __uint_as_float(u[2 * i]));
+      float h1 = silu_mul(__uint_as_float(g[2 * i + 1]), __uint_as_float(u[2 * i + 1]));
+      packed[i] = ptx::pack_bf16x2(h0, h1);
+    }
+    if (row_ok) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        if (col0 + c * 32 + v * 8 < p.I) {
+          uint4 w = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+          *reinterpret_cast<uint4 *>(orow + c * 32 + v * 8) = w;
+        }
+      }
+    }
+  }
+}
+
+// Phase B epilogue for one tile: out[row, col0 + j] = bf16(residual + acc_j), j < 256.
+__device__ __forceinline__ void epilogue_b(const Params &p, uint32_t taddr, uint32_t row, bool row_ok, uint32_t col0) {
+  __nv_bfloat16 *orow = p.out + static_cast<size_t>(row) * p.d + col0;
+  const __nv_bfloat16 *rrow = p.residual ? p.residual + static_cast<size_t>(row) * p.d + col0 : nullptr;
+#pragma unroll 1
+  for (uint32_t c = 0; c < UMMA_N / 32; ++c) {
+    uint32_t a[32];
+    ptx::tmem_ld_32x32b_x32(taddr + c * 32, a);
+    ptx::tmem_ld_wait();
+    if (row_ok) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const uint32_t col = col0 + c * 32 + v * 8;
+        if (col < p.d) {
+          float r[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          if (rrow) {
+            uint4 rv = *reinterpret_cast<const uint4 *>(rrow + c * 32 + v * 8);
+            const __nv_bfloat162 *r2 = reinterpret_cast<const __nv_bfloat162 *>(&rv);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float2 f = __bfloat1622float2(r2[e]);
+              r[2 * e] = f.x;
+              r[2 * e + 1] = f.y;
+            }
+          }
+          uint4 w;
+          w.x = ptx::pack_bf16x2(r[0] + __uint_as_float(a[8 * v + 0]), r[1] + __uint_as_float(a[8 * v + 1]));
+          w.y = ptx::pack_bf16x2(r[2] + __uint_as_float(a[8 * v + 2]), r[3] + __uint_as_float(a[8 * v + 3]));
+          w.z = ptx::pack_bf16x2(r[4] + __uint_as_float(a[8 * v + 4]), r[5] + __uint_as_float(a[8 * v + 5]));
+          w.w = ptx::pack_bf16x2(r[6] + __uint_as_float(a[8 * v + 6]), r[7] + __uint_as_float(a[8 * v + 7]));
+          *reinterpret_cast<uint4 *>(orow + c * 32 + v * 8) = w;
+        }
+      }
+    }
+  }
+}
+
+template <int CG, int MODE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    dual_b_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b0,
-                       const __grid_constant__ CUtensorMap tm_b1, const Params p) {
+    mlp_tc_kernel(const __grid_constant__ Maps maps, const Params p) {
   using C = Cfg<CG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment for the SWIZZLE_128B atoms
@@ -113,14 +242,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const bool leader = (rank == 0);
   const uint32_t cluster_id = blockIdx.x / CG;
   const uint32_t num_clusters = gridDim.x / CG;
-  const uint32_t num_tiles = p.m_tiles * p.n_tiles;
-  const uint32_t num_kb = (p.k + BK - 1) / BK;
-  constexpr uint32_t TILE_N = PHASE_A ? BHALF : UMMA_N;  // output columns per tile
+  const uint32_t num_tiles = num_tiles_of<MODE>(p);
+  const uint32_t kbA = (p.d + BK - 1) / BK;  // phase A reduces over hidden
+  const uint32_t kbB = (p.I + BK - 1) / BK;  // phase B reduces over intermediate
 
   if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tm_a);
-    ptx::prefetch_tmap(&tm_b0);
-    ptx::prefetch_tmap(&tm_b1);
+    if (MODE != MODE_B) {
+      ptx::prefetch_tmap(&maps.x);
+      ptx::prefetch_tmap(&maps.wg);
+      ptx::prefetch_tmap(&maps.wu);
+    }
+    if (MODE != MODE_A) {
+      ptx::prefetch_tmap(&maps.h);
+      ptx::prefetch_tmap(&maps.wd);
+    }
     for (uint32_t s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -142,18 +277,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     // ======================= TMA producer =======================
     if (lane == 0) {
-      const uint64_t pol_a = p.policy == 1 ? ptx::policy_evict_normal()
-                             : p.policy == 2 ? ptx::policy_evict_first()
-                             : (PHASE_A ? ptx::policy_evict_last() : ptx::policy_evict_normal());
-      const uint64_t pol_b = p.policy == 1 ? ptx::policy_evict_normal()
-                             : (PHASE_A ? ptx::policy_evict_normal() : ptx::policy_evict_last());
+      // L2 policies: phase A re-reads X rows across all N tiles of a group (keep), streams W;
+      // phase B keeps W_down (re-read by every row block), streams H.
+      const uint64_t pol_keep = ptx::policy_evict_last();
+      const uint64_t pol_norm = ptx::policy_evict_normal();
+      const uint64_t pol_first = ptx::policy_evict_first();
       const uint32_t full_leader0 = (CG == 2) ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : ptx::smem_u32(&full[0]);
       uint32_t stage = 0, phase = 0;
       for (uint32_t t = cluster_id; t < num_tiles; t += num_clusters) {
-        uint32_t mt, nt;
-        tile_coords(t, p, mt, nt);
-        const int32_t a_row = static_cast<int32_t>(mt * BM * CG + rank * BM);
-        const int32_t b_row0 = static_cast<int32_t>(nt * TILE_N);
+        const Tile tl = decode_tile<MODE>(t, p);
+        if (MODE == MODE_FUSED && !tl.a) {
+          // H rows of this CTA's 128-row block must be complete: wait for every phase-A tile
+          // of the block (released by their epilogues), then order the async-proxy (TMA) reads
+          // after that acquire.
+          const uint32_t *cnt = p.ready + tl.m * CG + rank;
+          while (ld_acquire_gpu(cnt) < p.nA) __nanosleep(128);
+          fence_proxy_async_global();
+        }
+        const CUtensorMap *ta = tl.a ? &maps.x : &maps.h;
+        const CUtensorMap *tb0 = tl.a ? &maps.wg : &maps.wd;
+        const CUtensorMap *tb1 = tl.a ? &maps.wu : &maps.wd;
+        const uint64_t pol_a = p.policy == 1 ? pol_norm : p.policy == 2 ? pol_first : (tl.a ? pol_keep : pol_norm);
+        const uint64_t pol_b = p.policy == 1 ? pol_norm : (tl.a ? pol_norm : pol_keep);
+        const int32_t a_row = static_cast<int32_t>(tl.m * BM * CG + rank * BM);
+        const int32_t b_row0 = static_cast<int32_t>(tl.a ? tl.n * BHALF : tl.n * UMMA_N);
+        const int32_t b_off1 = tl.a ? 0 : static_cast<int32_t>(BHALF);  // row offset of B half 1
+        const uint32_t num_kb = tl.a ? kbA : kbB;
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           const int32_t kc = static_cast<int32_t>(kb * BK);
@@ -162,15 +311,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t fbar = full_leader0 + stage * 8;
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], C::TX_BYTES);
           if constexpr (CG == 1) {
-            ptx::tma_load_2d(&tm_a, sa, fbar, kc, a_row, pol_a);
-            ptx::tma_load_2d(&tm_b0, sb, fbar, kc, b_row0, pol_b);
-            ptx::tma_load_2d(&tm_b1, sb + BHALF_BYTES, fbar, kc, b_row0 + (PHASE_A ? 0 : (int32_t)BHALF), pol_b);
+            ptx::tma_load_2d(ta, sa, fbar, kc, a_row, pol_a);
+            ptx::tma_load_2d(tb0, sb, fbar, kc, b_row0, pol_b);
+            ptx::tma_load_2d(tb1, sb + BHALF_BYTES, fbar, kc, b_row0 + b_off1, pol_b);
           } else {
-            ptx::tma_load_2d_cg2(&tm_a, sa, fbar, kc, a_row, pol_a);
+            ptx::tma_load_2d_cg2(ta, sa, fbar, kc, a_row, pol_a);
             if (rank == 0)
-              ptx::tma_load_2d_cg2(&tm_b0, sb, fbar, kc, b_row0, pol_b);
+              ptx::tma_load_2d_cg2(tb0, sb, fbar, kc, b_row0, pol_b);
             else
-              ptx::tma_load_2d_cg2(&tm_b1, sb, fbar, kc, b_row0 + (PHASE_A ? 0 : (int32_t)BHALF), pol_b);
+              ptx::tma_load_2d_cg2(tb1, sb, fbar, kc, b_row0 + b_off1, pol_b);
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -189,6 +338,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t stage = 0, phase = 0;
       uint32_t acc = 0, acc_phase = 0;
       for (uint32_t t = cluster_id; t < num_tiles; t += num_clusters) {
+        const Tile tl = decode_tile<MODE>(t, p);
+        const uint32_t num_kb = tl.a ? kbA : kbB;
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * ACC_COLS;
@@ -216,83 +367,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t acc = 0, acc_phase = 0;
     const uint32_t tempty_leader = (CG == 2) ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0;
     for (uint32_t t = cluster_id; t < num_tiles; t += num_clusters) {
-      uint32_t mt, nt;
-      tile_coords(t, p, mt, nt);
+      const Tile tl = decode_tile<MODE>(t, p);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const uint32_t row = mt * BM * CG + rank * BM + row_in_tile;
+      const uint32_t row = tl.m * BM * CG + rank * BM + row_in_tile;
       const bool row_ok = row < p.rows;
       const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * ACC_COLS;
-      const uint32_t col0 = nt * TILE_N;
-      if constexpr (PHASE_A) {
-        __nv_bfloat16 *orow = p.out + static_cast<size_t>(row) * p.ld_out + col0;
-        // folded RMSNorm (f3): gate/up of row r are scaled by r's 1/rms before the SiLU
-        const float rs = (p.row_scale != nullptr && row_ok) ? p.row_scale[row] : 1.0f;
-#pragma unroll 1
-        for (uint32_t c = 0; c < BHALF / 32; ++c) {
-          uint32_t g[32], u[32];
-          ptx::tmem_ld_32x32b_x32(taddr + c * 32, g);
-          ptx::tmem_ld_32x32b_x32(taddr + BHALF + c * 32, u);
-          ptx::tmem_ld_wait();
-          if (p.row_scale != nullptr) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              g[i] = __float_as_uint(__uint_as_float(g[i]) * rs);
-              u[i] = __float_as_uint(__uint_as_float(u[i]) * rs);
-            }
-          }
-          uint32_t packed[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float h0 = silu_mul(__uint_as_float(g[2 * i]), __uint_as_float(u[2 * i]));
-            float h1 = silu_mul(__uint_as_float(g[2 * i + 1]), __uint_as_float(u[2 * i + 1]));
-            packed[i] = ptx::pack_bf16x2(h0, h1);
-          }
-          if (row_ok) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              if (col0 + c * 32 + v * 8 < p.n_out) {
-                uint4 w = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
-                *reinterpret_cast<uint4 *>(orow + c * 32 + v * 8) = w;
-              }
-            }
-          }
-        }
-      } else {
-        __nv_bfloat16 *orow = p.out + static_cast<size_t>(row) * p.ld_out + col0;
-        const __nv_bfloat16 *rrow = p.residual ? p.residual + static_cast<size_t>(row) * p.ld_out + col0 : nullptr;
-#pragma unroll 1
-        for (uint32_t c = 0; c < UMMA_N / 32; ++c) {
-          uint32_t a[32];
-          ptx::tmem_ld_32x32b_x32(taddr + c * 32, a);
-          ptx::tmem_ld_wait();
-          if (row_ok) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const uint32_t col = col0 + c * 32 + v * 8;
-              if (col < p.n_out) {
-                float r[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                if (rrow) {
-                  uint4 rv = *reinterpret_cast<const uint4 *>(rrow + c * 32 + v * 8);
-                  const __nv_bfloat162 *r2 = reinterpret_cast<const __nv_bfloat162 *>(&rv);
-#pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    float2 f = __bfloat1622float2(r2[e]);
-                    r[2 * e] = f.x;
-                    r[2 * e + 1] = f.y;
-                  }
-                }
-                uint4 w;
-                w.x = ptx::pack_bf16x2(r[0] + __uint_as_float(a[8 * v + 0]), r[1] + __uint_as_float(a[8 * v + 1]));
-                w.y = ptx::pack_bf16x2(r[2] + __uint_as_float(a[8 * v + 2]), r[3] + __uint_as_float(a[8 * v + 3]));
-                w.z = ptx::pack_bf16x2(r[4] + __uint_as_float(a[8 * v + 4]), r[5] + __uint_as_float(a[8 * v + 5]));
-                w.w = ptx::pack_bf16x2(r[6] + __uint_as_float(a[8 * v + 6]), r[7] + __uint_as_float(a[8 * v + 7]));
-                *reinterpret_cast<uint4 *>(orow + c * 32 + v * 8) = w;
-              }
-            }
-          }
-        }
-      }
+      if (tl.a)
+        epilogue_a(p, taddr, row, row_ok, tl.n * BHALF);
+      else
+        epilogue_b(p, taddr, row, row_ok, tl.n * UMMA_N);
       // release the accumulator to the MMA issuer
       ptx::tc_fence_before();
       __syncwarp();
@@ -303,6 +387,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::mbar_arrive(&tempty[acc]);
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (MODE == MODE_FUSED && tl.a) {
+        // publish this tile's H rows: generic stores -> async proxy (TMA) of other CTAs
+        fence_proxy_async_global();
+        ptx::named_bar_sync(1, 128);  // all 4 epilogue warps of this CTA have stored
+        if (q == 0 && lane == 0) {
+          __threadfence();
+          atomicAdd(p.ready + tl.m * CG + rank, 1u);
+        }
+      }
     }
   }
 
@@ -314,12 +407,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-template <int CG, bool PHASE_A>
-static cudaError_t launch(const CUtensorMap &tm_a, const CUtensorMap &tm_b0, const CUtensorMap &tm_b1,
-                          const Params &p, int num_sms, cudaStream_t stream) {
+template <int CG, int MODE>
+static cudaError_t launch(const Maps &maps, const Params &p, int num_sms, cudaStream_t stream) {
   using C = Cfg<CG>;
-  auto kfn = dual_b_gemm_kernel<CG, PHASE_A>;
-  static thread_local int configured_device = -1;  // attribute is per device; cheap to re-set
+  auto kfn = mlp_tc_kernel<CG, MODE>;
+  static thread_local int configured_device = -1;  // attribute is per device
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -328,7 +420,7 @@ static cudaError_t launch(const CUtensorMap &tm_a, const CUtensorMap &tm_b0, con
     if (e != cudaSuccess) return e;
     configured_device = dev;
   }
-  const uint32_t num_tiles = p.m_tiles * p.n_tiles;
+  const uint32_t num_tiles = num_tiles_of<MODE>(p);
   uint32_t clusters = static_cast<uint32_t>(num_sms) / CG;
   if (clusters > num_tiles) clusters = num_tiles;
   if (clusters == 0) clusters = 1;
@@ -344,45 +436,48 @@ static cudaError_t launch(const CUtensorMap &tm_a, const CUtensorMap &tm_b0, con
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kfn, tm_a, tm_b0, tm_b1, p);
+  return cudaLaunchKernelEx(&cfg, kfn, maps, p);
+}
+
+template <int MODE>
+static cudaError_t launch_mode(const TcMlpArgs &a, cudaStream_t stream) {
+  Maps maps;
+  maps.x = *a.tm_x;
+  maps.wg = *a.tm_wg;
+  maps.wu = *a.tm_wu;
+  maps.h = *a.tm_h;
+  maps.wd = *a.tm_wd;
+  Params p{};
+  p.rows = a.rows;
+  p.d = a.d;
+  p.I = a.I;
+  p.m_tiles = (a.rows + BM * a.cta_group - 1) / (BM * a.cta_group);
+  p.nA = (a.I + BHALF - 1) / BHALF;
+  p.nB = (a.d + UMMA_N - 1) / UMMA_N;
+  // raster groups (energy sweep r1): 16 row blocks for phase A (X rows stay in L2), 8 for B
+  uint32_t g = a.group_m ? a.group_m : (MODE == MODE_B ? 8 : 16);
+  if (g > p.m_tiles) g = p.m_tiles;
+  p.group_m = g;
+  p.policy = a.policy;
+  p.h = a.h;
+  p.out = a.out;
+  p.residual = a.residual;
+  p.row_scale = a.row_scale;
+  p.ready = a.ready;
+  if (a.cta_group == 2) return launch<2, MODE>(maps, p, a.num_sms, stream);
+  return launch<1, MODE>(maps, p, a.num_sms, stream);
 }
 
 }  // namespace tc
 
-cudaError_t launch_phase_a_tc(const TcPhaseArgs &a, cudaStream_t stream) {
-  tc::Params p{};
-  p.rows = a.rows;
-  p.n_out = a.n_out;
-  p.k = a.k;
-  p.m_tiles = (a.rows + tc::BM * a.cta_group - 1) / (tc::BM * a.cta_group);
-  p.n_tiles = (a.n_out + tc::BHALF - 1) / tc::BHALF;
-  p.group_m = a.group_m ? a.group_m : 16;  // 16 x 256 rows: X rows of a group stay in L2 (energy sweep r1)
-  if (p.group_m > p.m_tiles) p.group_m = p.m_tiles;
-  p.out = a.out;
-  p.residual = nullptr;
-  p.ld_out = a.ld_out;
-  p.policy = a.policy;
-  p.row_scale = a.row_scale;
-  if (a.cta_group == 2) return tc::launch<2, true>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
-  return tc::launch<1, true>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
+cudaError_t launch_mlp_tc(const TcMlpArgs &a, int mode, cudaStream_t stream) {
+  switch (mode) {
+    case 0: return tc::launch_mode<tc::MODE_A>(a, stream);
+    case 1: return tc::launch_mode<tc::MODE_B>(a, stream);
+    default: return tc::launch_mode<tc::MODE_FUSED>(a, stream);
+  }
 }
 
-cudaError_t launch_phase_b_tc(const TcPhaseArgs &a, cudaStream_t stream) {
-  tc::Params p{};
-  p.rows = a.rows;
-  p.n_out = a.n_out;
-  p.k = a.k;
-  p.m_tiles = (a.rows + tc::BM * a.cta_group - 1) / (tc::BM * a.cta_group);
-  p.n_tiles = (a.n_out + tc::UMMA_N - 1) / tc::UMMA_N;
-  p.group_m = a.group_m ? a.group_m : 8;
-  if (p.group_m > p.m_tiles) p.group_m = p.m_tiles;
-  p.out = a.out;
-  p.residual = a.residual;
-  p.ld_out = a.ld_out;
-  p.policy = a.policy;
-  p.row_scale = a.row_scale;
-  if (a.cta_group == 2) return tc::launch<2, false>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
-  return tc::launch<1, false>(*a.tm_a, *a.tm_b0, *a.tm_b1, p, a.num_sms, stream);
-}
+size_t mlp_tc_ready_counters(uint32_t rows) { return (rows + tc::BM - 1) / tc::BM + 2; }
 
 }  // namespace mom

@@ -70,7 +70,9 @@ def test_workspace_is_one_minisequence(lib):
     g1 = GOLD["eq1_bytes"]  # C >= S: the unchunked Eq. 1 S*I*w
     assert lib.mom_mlp_minseq_workspace_bytes(g1["S"], 64, g1["I"], 10**9, _mom.MOM_F32) == g1["expect"]
     # config 2 (Llama MLP, S=65536, M=8, bf16): 8192 * 14336 * 2 bytes = 235 MB vs 1.88 GB
-    assert lib.mom_mlp_minseq_workspace_bytes(65536, 4096, 14336, 8192, _mom.MOM_BF16) == 8192 * 14336 * 2
+    # bf16 adds the fused kernel's per-row-block counters: a few hundred bytes
+    extra = lib.mom_mlp_minseq_workspace_bytes(65536, 4096, 14336, 8192, _mom.MOM_BF16) - 8192 * 14336 * 2
+    assert 0 < extra <= 4096
     assert lib.mom_mlp_minseq_workspace_bytes(0, 4096, 14336, 8192, _mom.MOM_BF16) == 0
 
 

@@ -70,7 +70,8 @@ def main():
         per = {}
         for k, t in timer.results():
             per.setdefault(k, []).append(t)
-        mlp_ms = (sum(per.get("phaseA_tc", [])) + sum(per.get("phaseB_tc", []))) / args.steps
+        mlp_ms = (sum(per.get("phaseA_tc", [])) + sum(per.get("phaseB_tc", [])) +
+                  sum(per.get("mlp_fused_tc", []))) / args.steps
         flops = 6.0 * S * d * I * (L - 1)
         out[mode] = {"ms_per_step": ms, "tokens_per_s": S / (ms * 1e-3), "mlp_ms": mlp_ms,
                      "mlp_tflops": flops / (mlp_ms * 1e-3) / 1e12,
