@@ -236,7 +236,10 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
   const uint32_t group_a = static_cast<uint32_t>(env_int("MOM_GROUP_M_A", 0));
   const uint32_t group_b = static_cast<uint32_t>(env_int("MOM_GROUP_M_B", 0));
   const uint32_t policy = static_cast<uint32_t>(env_int("MOM_TMA_POLICY", 0));
-  const bool fused = env_int("MOM_FUSED", 1) != 0;
+  // Two launches per mini-sequence by default: the fused single launch removes the inter-phase
+  // tail but runs phase-A and phase-B tiles concurrently, which costs more DRAM traffic, and on
+  // the power-capped B200 that energy costs more clock than the tail (energy sweep, round 1).
+  const bool fused = env_int("MOM_FUSED", 0) != 0;
   CUtensorMap tm_wg, tm_wu, tm_wd;
   mom_status_t st;
   if (dt == MOM_BF16) {

@@ -102,15 +102,42 @@ __device__ __forceinline__ Tile decode_tile(uint32_t t, const Params &p) {
   Tile tl;
   const uint32_t G = p.group_m;
   if constexpr (MODE == MODE_FUSED) {
-    const uint32_t per_group = G * (p.nA + p.nB);
-    const uint32_t g = t / per_group;
-    uint32_t local = t - g * per_group;
-    const uint32_t m0 = g * G;
-    uint32_t gm = p.m_tiles - m0;
-    if (gm > G) gm = G;
-    tl.a = local < gm * p.nA;
-    if (!tl.a) local -= gm * p.nA;
-    tl.m = m0 + local % gm;
+    // Lagged order A0, (A1, B0), (A2, B1), ..., (A_{ng-1}, B_{ng-2}), B_{ng-1}: the phase-B tiles
+    // of group g follow the phase-A tiles of group g+1, so by the time a CTA reaches them the
+    // phase-A tiles they depend on finished long ago (no bubble at group boundaries).
+    // Groups hold G row blocks except the last (rem = m_tiles % G); G <= m_tiles.
+    const uint32_t full = p.m_tiles / G, rem = p.m_tiles % G;
+    const uint32_t sA = G * p.nA, sB = G * p.nB;
+    uint32_t g, gm, local;
+    bool a;
+    if (t < sA) {
+      g = 0; gm = G; local = t; a = true;                          // A0
+    } else {
+      t -= sA;
+      const uint32_t P = sA + sB;
+      const uint32_t k = t / P;
+      if (k + 1 < full) {                                          // regular pair (A_{k+1}, B_k)
+        local = t - k * P;
+        a = local < sA;
+        g = a ? k + 1 : k;
+        if (!a) local -= sA;
+        gm = G;
+      } else {
+        t -= (full - 1) * P;
+        if (rem > 0 && t < rem * p.nA) {                           // A_full (partial)
+          g = full; gm = rem; local = t; a = true;
+        } else {
+          if (rem > 0) t -= rem * p.nA;
+          if (t < sB) {                                            // B_{full-1}
+            g = full - 1; gm = G; local = t; a = false;
+          } else {                                                 // B_full (partial)
+            g = full; gm = rem; local = t - sB; a = false;
+          }
+        }
+      }
+    }
+    tl.a = a;
+    tl.m = g * G + local % gm;
     tl.n = local / gm;
   } else {
     const uint32_t nt = MODE == MODE_A ? p.nA : p.nB;
@@ -297,8 +324,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const CUtensorMap *ta = tl.a ? &maps.x : &maps.h;
         const CUtensorMap *tb0 = tl.a ? &maps.wg : &maps.wd;
         const CUtensorMap *tb1 = tl.a ? &maps.wu : &maps.wd;
-        const uint64_t pol_a = p.policy == 1 ? pol_norm : p.policy == 2 ? pol_first : (tl.a ? pol_keep : pol_norm);
-        const uint64_t pol_b = p.policy == 1 ? pol_norm : (tl.a ? pol_norm : pol_keep);
+        uint64_t pol_a, pol_b;
+        switch (p.policy) {
+          case 1: pol_a = pol_norm; pol_b = pol_norm; break;                          // all normal
+          case 2: pol_a = pol_first; pol_b = tl.a ? pol_norm : pol_keep; break;      // A streamed
+          case 3: pol_a = tl.a ? pol_keep : pol_norm; pol_b = pol_first; break;      // weights streamed
+          case 4: pol_a = pol_keep; pol_b = pol_first; break;                        // A kept, W streamed
+          case 5: pol_a = tl.a ? pol_keep : pol_first; pol_b = tl.a ? pol_norm : pol_keep; break;  // H streamed
+          default: pol_a = tl.a ? pol_keep : pol_norm; pol_b = tl.a ? pol_norm : pol_keep; break;
+        }
         const int32_t a_row = static_cast<int32_t>(tl.m * BM * CG + rank * BM);
         const int32_t b_row0 = static_cast<int32_t>(tl.a ? tl.n * BHALF : tl.n * UMMA_N);
         const int32_t b_off1 = tl.a ? 0 : static_cast<int32_t>(BHALF);  // row offset of B half 1
