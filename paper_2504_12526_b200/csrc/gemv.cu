@@ -1,7 +1,8 @@
 // gemv.cu -- HBM-streaming kernels of MOM's last-token path (Alg. 1):
 //   * last_token_mlp: O_last = residual + W_down (Swish(W_gate x) (.) W_up x)
 //       kernel 1 streams W_gate and W_up (2*I*d*w bytes), keeps h in fp32;
-//       kernel 2 streams W_down (d*I*w bytes) with h staged in shared memory.
+//       kernel 2 streams W_down (d*I*w bytes), launched with PDL: it prefetches its W_down
+//       rows into L2 while kernel 1 runs, then waits (griddepcontrol) and reads h via L1.
 //   * lm_head: logits = W_head . rmsnorm(h) and the greedy token
 //       streams W_head (V*d*w bytes) once; per-block packed (value, index) maxima, then a
 //       one-block reduction.  Ties -> lowest index.
@@ -11,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -81,6 +83,80 @@ __device__ __forceinline__ float row_dot(const void *wrow, const float *xs, int 
   return warp_sum(acc);
 }
 
+// Two rows (gate and up) against the same smem vector, their loads interleaved so each lane
+// keeps 2 * UNROLL 16-B requests in flight.
+template <bool BF16>
+__device__ __forceinline__ void row_dot2(const void *wrow0, const void *wrow1, const float *xs, int n, int lane,
+                                         float &out0, float &out1) {
+  constexpr int EPV = BF16 ? 8 : 4;
+  const int nvec = n / EPV;
+  const uint4 *w0 = reinterpret_cast<const uint4 *>(wrow0);
+  const uint4 *w1 = reinterpret_cast<const uint4 *>(wrow1);
+  float a0 = 0.f, a1 = 0.f;
+  int v0 = 0;
+  for (; v0 + 32 * UNROLL <= nvec; v0 += 32 * UNROLL) {
+    uint4 b0[UNROLL], b1[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      b0[u] = ld_stream(w0 + v0 + u * 32 + lane);
+      b1[u] = ld_stream(w1 + v0 + u * 32 + lane);
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int e = (v0 + u * 32 + lane) * EPV;
+      a0 += BF16 ? dot8_bf16(b0[u], xs + e) : dot4_f32(b0[u], xs + e);
+      a1 += BF16 ? dot8_bf16(b1[u], xs + e) : dot4_f32(b1[u], xs + e);
+    }
+  }
+  for (int v = v0 + lane; v < nvec; v += 32) {
+    const int e = v * EPV;
+    const uint4 c0 = ld_stream(w0 + v), c1 = ld_stream(w1 + v);
+    a0 += BF16 ? dot8_bf16(c0, xs + e) : dot4_f32(c0, xs + e);
+    a1 += BF16 ? dot8_bf16(c1, xs + e) : dot4_f32(c1, xs + e);
+  }
+  out0 = warp_sum(a0);
+  out1 = warp_sum(a1);
+}
+
+// Dot of one weight row with an fp32 vector read through the read-only/L1 path (no smem
+// staging: every block starts streaming weights immediately).
+template <bool BF16>
+__device__ __forceinline__ float row_dot_gvec(const void *wrow, const float *__restrict__ hv, int n, int lane) {
+  constexpr int EPV = BF16 ? 8 : 4;
+  const int nvec = n / EPV;
+  const uint4 *w = reinterpret_cast<const uint4 *>(wrow);
+  float acc = 0.f;
+  int v0 = 0;
+  for (; v0 + 32 * UNROLL <= nvec; v0 += 32 * UNROLL) {
+    uint4 buf[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) buf[u] = ld_stream(w + v0 + u * 32 + lane);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int e = (v0 + u * 32 + lane) * EPV;
+      float xv[EPV];
+#pragma unroll
+      for (int q = 0; q < EPV / 4; ++q) {
+        const float4 f = __ldg(reinterpret_cast<const float4 *>(hv + e) + q);
+        xv[4 * q] = f.x; xv[4 * q + 1] = f.y; xv[4 * q + 2] = f.z; xv[4 * q + 3] = f.w;
+      }
+      acc += BF16 ? dot8_bf16(buf[u], xv) : dot4_f32(buf[u], xv);
+    }
+  }
+  for (int v = v0 + lane; v < nvec; v += 32) {
+    const uint4 b = ld_stream(w + v);
+    const int e = v * EPV;
+    float xv[EPV];
+#pragma unroll
+    for (int q = 0; q < EPV / 4; ++q) {
+      const float4 f = __ldg(reinterpret_cast<const float4 *>(hv + e) + q);
+      xv[4 * q] = f.x; xv[4 * q + 1] = f.y; xv[4 * q + 2] = f.z; xv[4 * q + 3] = f.w;
+    }
+    acc += BF16 ? dot8_bf16(b, xv) : dot4_f32(b, xv);
+  }
+  return warp_sum(acc);
+}
+
 template <bool BF16>
 __device__ __forceinline__ float load_elem(const void *p, size_t i) {
   if (BF16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16 *>(p)[i]);
@@ -94,37 +170,90 @@ __device__ __forceinline__ void store_elem(void *p, size_t i, float v) {
     reinterpret_cast<float *>(p)[i] = v;
 }
 
+// Stage n elements (n % elements-per-16B == 0) of a bf16/fp32 vector into shared memory as fp32
+// with independent 16-B loads (one round trip, not n/THREADS dependent ones); returns this
+// thread's partial sum of squares.
+template <bool BF16>
+__device__ __forceinline__ float stage_vec(const void *src, float *dst, int n) {
+  constexpr int EPV = BF16 ? 8 : 4;
+  const uint4 *s = reinterpret_cast<const uint4 *>(src);
+  float ss = 0.f;
+#pragma unroll 4
+  for (int v = threadIdx.x; v < n / EPV; v += THREADS) {
+    const uint4 q = s[v];
+    float f[EPV];
+    if constexpr (BF16) {
+      const __nv_bfloat162 *q2 = reinterpret_cast<const __nv_bfloat162 *>(&q);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 t = __bfloat1622float2(q2[e]);
+        f[2 * e] = t.x;
+        f[2 * e + 1] = t.y;
+      }
+    } else {
+      f[0] = __uint_as_float(q.x); f[1] = __uint_as_float(q.y); f[2] = __uint_as_float(q.z); f[3] = __uint_as_float(q.w);
+    }
+#pragma unroll
+    for (int e = 0; e < EPV; ++e) {
+      dst[v * EPV + e] = f[e];
+      ss = fmaf(f[e], f[e], ss);
+    }
+  }
+  return ss;
+}
+
+// Programmatic dependent launch (PDL): the primary lets the next kernel in the stream launch
+// early; the dependent prefetches its weight rows into L2 (they do not depend on the primary)
+// and only then waits for the primary grid's results.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// Prefetch (into L2) the weight rows this block's warps will stream: rows w, w + stride, ...
+__device__ __forceinline__ void prefetch_my_rows(const void *base, size_t pitch, int rows, int max_rows_per_warp) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * WARPS + (threadIdx.x >> 5);
+  if (lane < max_rows_per_warp) {
+    const int r = w + lane * gridDim.x * WARPS;
+    if (r < rows) prefetch_l2_bulk(static_cast<const char *>(base) + r * pitch, static_cast<uint32_t>(pitch));
+  }
+}
+
 // h[j] = Swish(sum_k x_k Wg[j,k]) * (sum_k x_k Wu[j,k]), fp32.  Grid-stride over rows j.
 template <bool BF16>
 __global__ void __launch_bounds__(THREADS) gate_up_gemv(const void *__restrict__ x, const void *__restrict__ wg,
                                                         const void *__restrict__ wu, float *__restrict__ h, int d,
                                                         int I) {
+  pdl_launch_dependents();  // the down GEMV may launch now and prefetch W_down
   extern __shared__ float xs[];
-  for (int k = threadIdx.x; k < d; k += THREADS) xs[k] = load_elem<BF16>(x, k);
+  stage_vec<BF16>(x, xs, d);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int w = blockIdx.x * WARPS + (threadIdx.x >> 5);
   const size_t pitch = static_cast<size_t>(d) * (BF16 ? 2 : 4);
   for (int j = w; j < I; j += gridDim.x * WARPS) {
-    const float g = row_dot<BF16>(static_cast<const char *>(wg) + j * pitch, xs, d, lane);
-    const float u = row_dot<BF16>(static_cast<const char *>(wu) + j * pitch, xs, d, lane);
+    float g, u;
+    row_dot2<BF16>(static_cast<const char *>(wg) + j * pitch, static_cast<const char *>(wu) + j * pitch, xs, d,
+                   lane, g, u);
     if (lane == 0) h[j] = g / (1.0f + __expf(-g)) * u;
   }
 }
 
-// out[c] = residual[c] + sum_j h_j Wd[c,j].  h (fp32) staged in shared memory.
+// out[c] = residual[c] + sum_j h_j Wd[c,j].  h (fp32) read through L1 (no staging barrier).
 template <bool BF16>
 __global__ void __launch_bounds__(THREADS) down_gemv(const float *__restrict__ h, const void *__restrict__ wd,
                                                      const void *__restrict__ residual, void *__restrict__ out, int d,
-                                                     int I) {
-  extern __shared__ float hs[];
-  for (int j = threadIdx.x; j < I; j += THREADS) hs[j] = h[j];
-  __syncthreads();
+                                                     int I, int prefetch_rows) {
   const int lane = threadIdx.x & 31;
   const int w = blockIdx.x * WARPS + (threadIdx.x >> 5);
   const size_t pitch = static_cast<size_t>(I) * (BF16 ? 2 : 4);
+  // W_down does not depend on h: pull this warp's rows towards L2 while gate/up still runs
+  if ((pitch & 15) == 0 && prefetch_rows > 0) prefetch_my_rows(wd, pitch, d, prefetch_rows);
+  pdl_launch_dependents();  // the LM head may launch early too
+  pdl_wait();               // h (written by gate_up_gemv) is complete and visible from here on
   for (int c = w; c < d; c += gridDim.x * WARPS) {
-    const float o = row_dot<BF16>(static_cast<const char *>(wd) + c * pitch, hs, I, lane);
+    const float o = row_dot_gvec<BF16>(static_cast<const char *>(wd) + c * pitch, h, I, lane);
     if (lane == 0) {
       const float r = residual ? load_elem<BF16>(residual, c) : 0.f;
       store_elem<BF16>(out, c, r + o);
@@ -159,13 +288,9 @@ __global__ void __launch_bounds__(THREADS) lm_head_gemv(const void *__restrict__
   extern __shared__ float hs[];
   __shared__ float red[WARPS];
   __shared__ unsigned long long best_s[WARPS];
+  pdl_wait();  // h comes from the previous kernel (PDL launch; a no-op without the attribute)
   // prologue: fp32 copy of h and (optionally) the final RMSNorm
-  float ss = 0.f;
-  for (int k = threadIdx.x; k < d; k += THREADS) {
-    const float v = load_elem<BF16>(hin, k);
-    hs[k] = v;
-    ss += v * v;
-  }
+  float ss = stage_vec<BF16>(hin, hs, d);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (gain) {
     ss = warp_sum(ss);
@@ -222,6 +347,36 @@ __global__ void key_to_index(const unsigned long long *__restrict__ key, int32_t
   out[0] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(key[0] & 0xFFFFFFFFull));
 }
 
+// Launch `kfn` on `stream` with programmatic stream serialization (PDL): it may start while
+// the previous kernel in the stream is still running; it synchronises with griddepcontrol.wait.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kfn)(KArgs...), int blocks, size_t smem, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks, 1, 1);
+  cfg.blockDim = dim3(THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kfn, static_cast<KArgs>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_maybe_pdl(void (*kfn)(KArgs...), int blocks, size_t smem, cudaStream_t stream, bool pdl,
+                                    Args... args) {
+  if (pdl) return launch_pdl(kfn, blocks, smem, stream, args...);
+  kfn<<<blocks, THREADS, smem, stream>>>(static_cast<KArgs>(args)...);
+  return cudaGetLastError();
+}
+
+static int env_or(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
 template <typename K>
 static cudaError_t set_smem(K kfn, size_t bytes) {
   if (bytes <= 48 * 1024) return cudaSuccess;
@@ -235,23 +390,29 @@ cudaError_t launch_last_token_mlp(const void *x, const void *residual, const voi
                                   cudaStream_t stream) {
   using namespace gemv;
   const size_t smem1 = static_cast<size_t>(d) * sizeof(float);
-  const size_t smem2 = static_cast<size_t>(I) * sizeof(float);
-  // kernel 1: 2 rows (gate+up) per warp per step; enough warps for several MB in flight
-  int blocks1 = (I + WARPS - 1) / WARPS;
-  if (blocks1 > num_sms * 8) blocks1 = num_sms * 8;
-  int blocks2 = (d + WARPS - 1) / WARPS;
-  if (blocks2 > num_sms * 4) blocks2 = num_sms * 4;
+  // Balanced single-wave grids: r = ceil(rows / resident warps) rows per warp, and just enough
+  // warps that every warp gets r rows (or r - 1 for the last ones) -- no half-empty second round.
+  auto balanced_blocks = [num_sms](int rows, int blocks_per_sm) {
+    const int resident = num_sms * blocks_per_sm * WARPS;
+    const int r = (rows + resident - 1) / resident;
+    const int warps = (rows + r - 1) / r;
+    return (warps + WARPS - 1) / WARPS;
+  };
+  const int blocks1 = balanced_blocks(I, 6);
+  const int blocks2 = balanced_blocks(d, 6);
+  const bool pdl = env_or("MOM_GEMV_PDL", 1) != 0;     // PDL launch of the down GEMV
+  const int pf = env_or("MOM_GEMV_PREFETCH", 0);        // W_down rows per warp prefetched to L2 first
   cudaError_t e;
   if (is_bf16) {
     if ((e = set_smem(gate_up_gemv<true>, smem1)) != cudaSuccess) return e;
-    if ((e = set_smem(down_gemv<true>, smem2)) != cudaSuccess) return e;
     gate_up_gemv<true><<<blocks1, THREADS, smem1, stream>>>(x, wg, wu, h_ws, d, I);
-    down_gemv<true><<<blocks2, THREADS, smem2, stream>>>(h_ws, wd, residual, out, d, I);
+    if ((e = launch_maybe_pdl(down_gemv<true>, blocks2, 0, stream, pdl, h_ws, wd, residual, out, d, I, pf)) != cudaSuccess)
+      return e;
   } else {
     if ((e = set_smem(gate_up_gemv<false>, smem1)) != cudaSuccess) return e;
-    if ((e = set_smem(down_gemv<false>, smem2)) != cudaSuccess) return e;
     gate_up_gemv<false><<<blocks1, THREADS, smem1, stream>>>(x, wg, wu, h_ws, d, I);
-    down_gemv<false><<<blocks2, THREADS, smem2, stream>>>(h_ws, wd, residual, out, d, I);
+    if ((e = launch_maybe_pdl(down_gemv<false>, blocks2, 0, stream, pdl, h_ws, wd, residual, out, d, I, pf)) != cudaSuccess)
+      return e;
   }
   return cudaGetLastError();
 }
@@ -270,10 +431,12 @@ cudaError_t launch_lm_head(const void *h, const void *gain, float eps, const voi
   cudaError_t e;
   if (is_bf16) {
     if ((e = set_smem(lm_head_gemv<true>, smem)) != cudaSuccess) return e;
-    lm_head_gemv<true><<<blocks, THREADS, smem, stream>>>(h, gain, eps, w, logits, partials, d, V, vocab_offset);
+    e = launch_pdl(lm_head_gemv<true>, blocks, smem, stream, h, gain, eps, w, logits, partials, d, V, vocab_offset);
+    if (e != cudaSuccess) return e;
   } else {
     if ((e = set_smem(lm_head_gemv<false>, smem)) != cudaSuccess) return e;
-    lm_head_gemv<false><<<blocks, THREADS, smem, stream>>>(h, gain, eps, w, logits, partials, d, V, vocab_offset);
+    e = launch_pdl(lm_head_gemv<false>, blocks, smem, stream, h, gain, eps, w, logits, partials, d, V, vocab_offset);
+    if (e != cudaSuccess) return e;
   }
   argmax_reduce<<<1, 1024, 0, stream>>>(partials, blocks, argmax, key_out);
   return cudaGetLastError();
