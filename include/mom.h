@@ -216,6 +216,29 @@ mom_status_t mom_kv_reload(const void *kv_host_pinned, void *kv_dev, size_t byte
  *                            shard is at row rank*rows_per_rank; in-place ncclAllGather on
  *                            `stream`; after completion every rank holds all rows.
  * ---------------------------------------------------------------------------------- */
+mom_status_t mom_nccl_barrier(void *comm, int32_t *scratch /* device int32[1] */, mom_stream_t stream);
+
+/* f1: the all-gather fused into the down-GEMM epilogue.  Same as
+ * mom_mlp_minseq_fwd, and every output row O_i is ALSO stored, from the phase-B epilogue
+ * that produces it, into each of the n_peers buffers peer_out[k] (same row offsets as `out`):
+ * the peers' gathered [N*S_local, hidden] buffers at this rank's shard, NVLink-mapped with
+ * mom_ipc_open_handle.  The rows cross NVLink while the tensor cores keep working, instead
+ * of in a separate collective after the layer.  After the call, one mom_nccl_barrier on
+ * the same stream orders every rank's peer stores before any rank's next layer.
+ *   0 <= n_peers <= 7; peer_out[k] 16-B aligned; bf16 only when n_peers > 0.
+ * IPC plumbing: mom_ipc_get_handle returns the 64-byte cudaIpcMemHandle of the allocation
+ * holding dev_ptr and dev_ptr's offset in it (torch sub-allocates); mom_ipc_open_handle maps
+ * a peer's handle (cudaIpcMemLazyEnablePeerAccess) and returns base + offset;
+ * mom_ipc_close unmaps it. */
+mom_status_t mom_mlp_minseq_fwd_gather(const void *x, const void *residual, const void *w_gate,
+                                       const void *w_up, const void *w_down, void *out,
+                                       void *const *peer_out, int n_peers, int64_t S, int64_t hidden,
+                                       int64_t intermediate, int64_t minseq_len, mom_dtype_t dt,
+                                       void *workspace, size_t workspace_bytes, mom_stream_t stream);
+mom_status_t mom_ipc_get_handle(const void *dev_ptr, void *handle_out /* 64 B */, int64_t *offset_out);
+mom_status_t mom_ipc_open_handle(const void *handle /* 64 B */, int64_t offset, void **dev_ptr_out);
+mom_status_t mom_ipc_close(void *dev_ptr, int64_t offset);
+
 mom_status_t mom_nccl_get_unique_id(void *id_out /* 128 bytes */);
 mom_status_t mom_nccl_comm_init(void **comm_out, int nranks, const void *id /* 128 B */, int rank);
 mom_status_t mom_nccl_comm_destroy(void *comm);

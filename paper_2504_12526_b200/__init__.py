@@ -18,11 +18,16 @@ from ._mom import (  # noqa: F401
     lm_head_last,
     mlp_last_token,
     fold_norm_gain,
+    ipc_close,
+    ipc_get_handle,
+    ipc_open_handle,
     mlp_minseq_fwd,
     mlp_minseq_fwd_from_host,
+    mlp_minseq_fwd_gather,
     mlp_minseq_rmsnorm_fwd,
     mlp_minseq_workspace_bytes,
     nccl_comm_destroy,
+    nccl_barrier,
     nccl_comm_init,
     nccl_get_unique_id,
     plan_minseq,

@@ -43,6 +43,12 @@ SIGNATURES = {
     "mom_nccl_comm_destroy": (_i32, [_p]),
     "mom_allgather_rows": (_i32, [_p, _i64, _i64, _i32, _p, _i32, _i32, _p]),
     "mom_set_timing_events": (_i32, [_p, _p, _i64, _p]),
+    "mom_nccl_barrier": (_i32, [_p, _p, _p]),
+    "mom_mlp_minseq_fwd_gather": (_i32, [_p, _p, _p, _p, _p, _p, _p, _i32, _i64, _i64, _i64, _i64, _i32, _p, _sz,
+                                         _p]),
+    "mom_ipc_get_handle": (_i32, [_p, _p, ctypes.POINTER(ctypes.c_int64)]),
+    "mom_ipc_open_handle": (_i32, [_p, _i64, ctypes.POINTER(ctypes.c_void_p)]),
+    "mom_ipc_close": (_i32, [_p, _i64]),
 }
 
 KIND_NAMES = {0: "phaseA_tc", 1: "phaseB_tc", 2: "phaseA_f32", 3: "phaseB_f32", 4: "last_token_gemv",
@@ -281,6 +287,47 @@ def kv_reload(kv_host_pinned, kv_dev, copy_stream=None, done=None, nbytes=None):
     if done is not None and ev is None:
         done.record(copy_stream if copy_stream is not None else torch.cuda.current_stream())
     return done
+
+
+def mlp_minseq_fwd_gather(x, residual, w_gate, w_up, w_down, out, peer_out, minseq_len: int, workspace=None,
+                          stream=None):
+    """f1: mlp_minseq_fwd whose phase-B epilogue also stores every output row into each peer
+    buffer (device pointers, e.g. from ipc_open_handle, offset like `out`)."""
+    S, hidden = x.shape
+    I = w_gate.shape[0]
+    dt = _dt(x)
+    if workspace is None:
+        nbytes = lib().mom_mlp_minseq_workspace_bytes(S, hidden, I, minseq_len, dt)
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    peers = [_ptr(p) for p in peer_out]
+    arr = (ctypes.c_void_p * max(1, len(peers)))(*peers)
+    _check(lib().mom_mlp_minseq_fwd_gather(_ptr(x), _ptr(residual), _ptr(w_gate), _ptr(w_up), _ptr(w_down), _ptr(out),
+                                           arr, len(peers), S, hidden, I, minseq_len, dt, _ptr(workspace),
+                                           workspace.numel() * workspace.element_size(), _stream(stream)))
+    return out
+
+
+def ipc_get_handle(t) -> tuple[bytes, int]:
+    """(64-byte cudaIpcMemHandle of t's allocation, byte offset of t in it)."""
+    buf = (ctypes.c_uint8 * 64)()
+    off = ctypes.c_int64(0)
+    _check(lib().mom_ipc_get_handle(_ptr(t), buf, ctypes.byref(off)))
+    return bytes(buf), off.value
+
+
+def ipc_open_handle(handle: bytes, offset: int) -> int:
+    buf = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    ptr = ctypes.c_void_p()
+    _check(lib().mom_ipc_open_handle(buf, offset, ctypes.byref(ptr)))
+    return ptr.value
+
+
+def ipc_close(ptr: int, offset: int):
+    _check(lib().mom_ipc_close(ptr, offset))
+
+
+def nccl_barrier(comm: int, scratch, stream=None):
+    _check(lib().mom_nccl_barrier(comm, _ptr(scratch), _stream(stream)))
 
 
 def nccl_get_unique_id() -> bytes:

@@ -227,7 +227,8 @@ mom_status_t validate_minseq(const char *who, const void *x, const void *residua
 mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate, const void *w_up,
                         const void *w_down, void *out, int64_t S, int64_t hidden, int64_t intermediate, int64_t C,
                         mom_dtype_t dt, void *workspace, cudaStream_t stream, const void *x_host,
-                        cudaStream_t copy, const float *norm_eps = nullptr) {
+                        cudaStream_t copy, const float *norm_eps = nullptr, void *const *peers = nullptr,
+                        int n_peers = 0) {
   int num_sms = 0;
   if (num_sms_current(&num_sms) != 0) return fail(MOM_ERR_CUDA, "mom_mlp_minseq_fwd: no CUDA device");
   const int64_t M = (S + C - 1) / C;  // Alg. 1
@@ -297,6 +298,8 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     a.h = h; a.out = static_cast<__nv_bfloat16 *>(oi); a.residual = static_cast<const __nv_bfloat16 *>(ri);
     a.cta_group = cta_group; a.policy = policy; a.num_sms = num_sms;
     a.ready = reinterpret_cast<uint32_t *>(static_cast<char *>(workspace) + h_bytes(S, intermediate, C, dt));
+    a.n_peers = static_cast<uint32_t>(n_peers);  // f1: O_i rows also stored into every peer's gathered buffer
+    for (int k = 0; k < n_peers; ++k) a.peer_out[k] = reinterpret_cast<__nv_bfloat16 *>(static_cast<char *>(peers[k]) + off);
     if (norm_eps) {
       // folded RMSNorm (f3): 1/rms of this mini-sequence's rows, after H_i and the counters
       float *inv = reinterpret_cast<float *>(static_cast<char *>(workspace) +
@@ -347,6 +350,71 @@ mom_status_t mom_mlp_minseq_fwd(const void *x, const void *residual, const void 
   if (st != MOM_OK) return st;
   return run_minseq(x, residual, w_gate, w_up, w_down, out, S, hidden, intermediate, C, dt, workspace,
                     static_cast<cudaStream_t>(stream), nullptr, nullptr);
+}
+
+mom_status_t mom_mlp_minseq_fwd_gather(const void *x, const void *residual, const void *w_gate, const void *w_up,
+                                       const void *w_down, void *out, void *const *peer_out, int n_peers, int64_t S,
+                                       int64_t hidden, int64_t intermediate, int64_t C, mom_dtype_t dt,
+                                       void *workspace, size_t workspace_bytes, mom_stream_t stream) {
+  g_err[0] = 0;
+  mom_status_t st = validate_minseq("mom_mlp_minseq_fwd_gather", x, residual, w_gate, w_up, w_down, out, S, hidden,
+                                    intermediate, C, dt, workspace, workspace_bytes);
+  if (st != MOM_OK) return st;
+  if (n_peers < 0 || n_peers > static_cast<int>(mom::kMaxPeers) || (n_peers > 0 && !peer_out))
+    return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd_gather: 0 <= n_peers <= %u", mom::kMaxPeers);
+  for (int k = 0; k < n_peers; ++k)
+    if (!peer_out[k] || !aligned16(peer_out[k]))
+      return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd_gather: peer %d pointer null or misaligned", k);
+  if (dt != MOM_BF16 && n_peers > 0)
+    return fail(MOM_ERR_UNSUPPORTED, "mom_mlp_minseq_fwd_gather: peer stores are bf16 (tcgen05 path) only");
+  return run_minseq(x, residual, w_gate, w_up, w_down, out, S, hidden, intermediate, C, dt, workspace,
+                    static_cast<cudaStream_t>(stream), nullptr, nullptr, nullptr, peer_out, n_peers);
+}
+
+mom_status_t mom_ipc_get_handle(const void *dev_ptr, void *handle_out, int64_t *offset_out) {
+  g_err[0] = 0;
+  if (!dev_ptr || !handle_out || !offset_out) return fail(MOM_ERR_INVALID_ARG, "mom_ipc_get_handle: null pointer");
+  // the IPC handle names the whole allocation: find its base (torch sub-allocates)
+  using RangeFn = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+  static RangeFn range = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    return (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+               ? reinterpret_cast<RangeFn>(p)
+               : nullptr;
+  }();
+  if (!range) return fail(MOM_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(MOM_ERR_INVALID_ARG, "mom_ipc_get_handle: not a device allocation");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  return MOM_OK;
+}
+
+mom_status_t mom_ipc_open_handle(const void *handle, int64_t offset, void **dev_ptr_out) {
+  g_err[0] = 0;
+  if (!handle || !dev_ptr_out || offset < 0) return fail(MOM_ERR_INVALID_ARG, "mom_ipc_open_handle: bad arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void *base = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  *dev_ptr_out = static_cast<char *>(base) + offset;
+  return MOM_OK;
+}
+
+mom_status_t mom_ipc_close(void *dev_ptr, int64_t offset) {
+  g_err[0] = 0;
+  if (!dev_ptr) return fail(MOM_ERR_INVALID_ARG, "mom_ipc_close: null pointer");
+  cudaError_t e = cudaIpcCloseMemHandle(static_cast<char *>(dev_ptr) - offset);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+  return MOM_OK;
 }
 
 mom_status_t mom_mlp_minseq_fwd_from_host(const void *x_host_pinned, void *x, const void *residual,
@@ -669,6 +737,18 @@ mom_status_t mom_allgather_rows(void *rows, int64_t rows_per_rank, int64_t hidde
   const void *send = static_cast<const char *>(rows) + static_cast<size_t>(rank) * count * w;  // in-place
   int rc = n.allgather(send, rows, count, nccl_dtype, comm, static_cast<cudaStream_t>(stream));
   if (rc != 0) return nccl_fail(rc, "ncclAllGather");
+  return MOM_OK;
+}
+
+mom_status_t mom_nccl_barrier(void *comm, int32_t *scratch, mom_stream_t stream) {
+  g_err[0] = 0;
+  if (!comm || !scratch) return fail(MOM_ERR_INVALID_ARG, "mom_nccl_barrier: null pointer");
+  Nccl &n = nccl();
+  if (!n.ok) return fail(MOM_ERR_NCCL, "%s", n.why);
+  // a 1-element all-reduce on `stream`: no rank's later work starts before every rank's earlier
+  // work on its stream (e.g. the peer stores of mom_mlp_minseq_fwd_gather) has completed
+  int rc = n.allreduce(scratch, scratch, 1, 2 /* ncclInt32 */, 0 /* ncclSum */, comm, static_cast<cudaStream_t>(stream));
+  if (rc != 0) return nccl_fail(rc, "ncclAllReduce(barrier)");
   return MOM_OK;
 }
 

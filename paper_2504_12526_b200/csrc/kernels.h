@@ -8,6 +8,8 @@
 
 namespace mom {
 
+constexpr uint32_t kMaxPeers = 7;  // f1: up to 8 GPUs (7 peers) receive every phase-B output row
+
 // One mini-sequence on the tcgen05 path (mlp_tc.cu).  Tensor maps are 2D bf16, box 64 x 128.
 struct TcMlpArgs {
   const CUtensorMap *tm_x;   // X_i [C_i, d]    (phase A operand A)
@@ -22,6 +24,8 @@ struct TcMlpArgs {
   const __nv_bfloat16 *residual;  // may be null
   const float *row_scale;    // folded RMSNorm 1/rms per row (phase A), or null
   uint32_t *ready;           // fused mode: mlp_tc_ready_counters(rows) zeroed counters
+  uint32_t n_peers;          // f1: number of peer destinations (<= kMaxPeers)
+  __nv_bfloat16 *peer_out[kMaxPeers];  // f1: peer gathered buffers at this mini-sequence's rows
   int cta_group;             // 1 or 2
   uint32_t group_m;          // raster group (0 = default)
   uint32_t policy;           // TMA L2 cache policy variant (0 = default)

@@ -66,7 +66,9 @@ struct Cfg {
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t STAGES = CG == 1 ? 4 : 6;
   static constexpr uint32_t TX_BYTES = STAGE_BYTES * CG;  // bytes landing per stage per tile
-  static constexpr uint32_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+  static constexpr uint32_t EPI_STAGE_BYTES = 4 * 32 * 128;  // phase-B epilogue: 32 rows x 128 B per warp
+  static constexpr uint32_t SMEM_BYTES =
+      1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/ + EPI_STAGE_BYTES;
 };
 
 // The five operands of one mini-sequence (unused ones are copies in single-phase modes).
@@ -90,6 +92,8 @@ struct Params {
   const __nv_bfloat16 *residual; // phase B residual, may be null
   const float *row_scale;        // phase A: folded-RMSNorm 1/rms per row, or null
   uint32_t *ready;               // MODE_FUSED: per (row block, CTA rank) count of finished phase-A tiles
+  uint32_t n_peers;              // f1: extra destinations of the phase-B output rows
+  __nv_bfloat16 *peer_out[kMaxPeers];  // f1: peers' gathered buffers, offset like `out`
 };
 
 struct Tile {
@@ -210,40 +214,82 @@ __device__ __forceinline__ void epilogue_a(const Params &p, uint32_t taddr, uint
   }
 }
 
-// Phase B epilogue for one tile: out[row, col0 + j] = bf16(residual + acc_j), j < 256.
-__device__ __forceinline__ void epilogue_b(const Params &p, uint32_t taddr, uint32_t row, bool row_ok, uint32_t col0) {
-  __nv_bfloat16 *orow = p.out + static_cast<size_t>(row) * p.d + col0;
-  const __nv_bfloat16 *rrow = p.residual ? p.residual + static_cast<size_t>(row) * p.d + col0 : nullptr;
+// Phase B epilogue for one tile: out[row, col0 + j] = bf16(residual + acc_j), j < 256, for the
+// 32 rows of this warp (TMEM lane quarter q), 64 columns (128 B per row) at a time.  Rows live
+// one per thread in TMEM, so the residual and the output go through a per-warp 32 x 128 B
+// shared-memory stage (16-B units XOR-swizzled by row: conflict-free both ways) and are moved
+// to/from global memory coalesced, 4 full 128-B row segments per warp instruction.  Every
+// output chunk is stored to `out` and to each peer's gathered buffer (f1: the all-gather of
+// token-sharded runs fused into this epilogue; peers are NVLink-mapped device pointers).
+__device__ __forceinline__ void epilogue_b(const Params &p, uint32_t taddr, uint32_t row0_warp, uint32_t col0,
+                                           uint8_t *stage) {
+  const uint32_t lane = ptx::lane_id();
+  const uint32_t sbase = ptx::smem_u32(stage);
+  // 16-B unit v of row r of the stage lives at byte r*128 + ((v ^ r) & 7) * 16
+  auto sw = [&](uint32_t r, uint32_t v) { return sbase + r * 128 + (((v ^ r) & 7) << 4); };
+  const uint32_t cr = lane >> 3, cv = lane & 7;  // coalesced mapping: lane -> (row cr + 4i, unit cv)
 #pragma unroll 1
-  for (uint32_t c = 0; c < UMMA_N / 32; ++c) {
-    uint32_t a[32];
-    ptx::tmem_ld_32x32b_x32(taddr + c * 32, a);
+  for (uint32_t c = 0; c < UMMA_N / 64; ++c) {
+    const uint32_t ccol = col0 + c * 64;  // first column of this chunk
+    uint32_t a[64];
+    ptx::tmem_ld_32x32b_x32(taddr + c * 64, *reinterpret_cast<uint32_t(*)[32]>(a));
+    ptx::tmem_ld_32x32b_x32(taddr + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(a + 32));
+    // residual chunk -> stage (coalesced global reads)
+    if (p.residual) {
+#pragma unroll
+      for (uint32_t i = 0; i < 8; ++i) {
+        const uint32_t r = cr + 4 * i, grow = row0_warp + r, gcol = ccol + cv * 8;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (grow < p.rows && gcol < p.d) v = *reinterpret_cast<const uint4 *>(p.residual + size_t(grow) * p.d + gcol);
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sw(r, cv)), "r"(v.x), "r"(v.y), "r"(v.z),
+                     "r"(v.w)
+                     : "memory");
+      }
+      __syncwarp();
+    }
     ptx::tmem_ld_wait();
-    if (row_ok) {
+    // this thread's row: add residual in fp32, one RNE rounding, back into the stage
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const uint32_t col = col0 + c * 32 + v * 8;
-        if (col < p.d) {
-          float r[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          if (rrow) {
-            uint4 rv = *reinterpret_cast<const uint4 *>(rrow + c * 32 + v * 8);
-            const __nv_bfloat162 *r2 = reinterpret_cast<const __nv_bfloat162 *>(&rv);
+    for (uint32_t v = 0; v < 8; ++v) {
+      float r[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (p.residual) {
+        uint4 q;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
+                     : "r"(sw(lane, v))
+                     : "memory");
+        const __nv_bfloat162 *q2 = reinterpret_cast<const __nv_bfloat162 *>(&q);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              float2 f = __bfloat1622float2(r2[e]);
-              r[2 * e] = f.x;
-              r[2 * e + 1] = f.y;
-            }
-          }
-          uint4 w;
-          w.x = ptx::pack_bf16x2(r[0] + __uint_as_float(a[8 * v + 0]), r[1] + __uint_as_float(a[8 * v + 1]));
-          w.y = ptx::pack_bf16x2(r[2] + __uint_as_float(a[8 * v + 2]), r[3] + __uint_as_float(a[8 * v + 3]));
-          w.z = ptx::pack_bf16x2(r[4] + __uint_as_float(a[8 * v + 4]), r[5] + __uint_as_float(a[8 * v + 5]));
-          w.w = ptx::pack_bf16x2(r[6] + __uint_as_float(a[8 * v + 6]), r[7] + __uint_as_float(a[8 * v + 7]));
-          *reinterpret_cast<uint4 *>(orow + c * 32 + v * 8) = w;
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(q2[e]);
+          r[2 * e] = f.x;
+          r[2 * e + 1] = f.y;
         }
       }
+      const uint32_t w0 = ptx::pack_bf16x2(r[0] + __uint_as_float(a[8 * v + 0]), r[1] + __uint_as_float(a[8 * v + 1]));
+      const uint32_t w1 = ptx::pack_bf16x2(r[2] + __uint_as_float(a[8 * v + 2]), r[3] + __uint_as_float(a[8 * v + 3]));
+      const uint32_t w2 = ptx::pack_bf16x2(r[4] + __uint_as_float(a[8 * v + 4]), r[5] + __uint_as_float(a[8 * v + 5]));
+      const uint32_t w3 = ptx::pack_bf16x2(r[6] + __uint_as_float(a[8 * v + 6]), r[7] + __uint_as_float(a[8 * v + 7]));
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sw(lane, v)), "r"(w0), "r"(w1), "r"(w2), "r"(w3)
+                   : "memory");
     }
+    __syncwarp();
+    // stage -> out (+ peers), coalesced: 4 rows x 128 B per warp instruction
+#pragma unroll
+    for (uint32_t i = 0; i < 8; ++i) {
+      const uint32_t r = cr + 4 * i, grow = row0_warp + r, gcol = ccol + cv * 8;
+      uint4 v;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                   : "r"(sw(r, cv))
+                   : "memory");
+      if (grow < p.rows && gcol < p.d) {
+        const size_t off = size_t(grow) * p.d + gcol;
+        *reinterpret_cast<uint4 *>(p.out + off) = v;
+        for (uint32_t k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint4 *>(p.peer_out[k] + off) = v;
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -262,6 +308,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t *tfull = bars + 2 * C::STAGES;      // [2]
   uint64_t *tempty = bars + 2 * C::STAGES + 2; // [2]
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * C::STAGES + 4);
+  uint8_t *epi_stage = smem + C::STAGES * C::STAGE_BYTES + 256;  // phase-B epilogue staging, 4 x 4 KB
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
@@ -410,7 +457,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (tl.a)
         epilogue_a(p, taddr, row, row_ok, tl.n * BHALF);
       else
-        epilogue_b(p, taddr, row, row_ok, tl.n * UMMA_N);
+        epilogue_b(p, taddr, row - lane, tl.n * UMMA_N, epi_stage + q * 32 * 128);
       // release the accumulator to the MMA issuer
       ptx::tc_fence_before();
       __syncwarp();
@@ -498,6 +545,8 @@ static cudaError_t launch_mode(const TcMlpArgs &a, cudaStream_t stream) {
   p.residual = a.residual;
   p.row_scale = a.row_scale;
   p.ready = a.ready;
+  p.n_peers = a.n_peers;
+  for (uint32_t k = 0; k < a.n_peers && k < kMaxPeers; ++k) p.peer_out[k] = a.peer_out[k];
   if (a.cta_group == 2) return launch<2, MODE>(maps, p, a.num_sms, stream);
   return launch<1, MODE>(maps, p, a.num_sms, stream);
 }
