@@ -59,6 +59,8 @@ def parse_args():
     ap.add_argument("--config", type=int, default=1, help="index into BASELINE.json configs (default 1 = config 2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gather", choices=["fused", "nccl"], default="fused",
+                    help="N>1: all-gather fused into the down-GEMM epilogue (f1) or a separate ncclAllGather")
     return ap.parse_args()
 
 
@@ -179,6 +181,27 @@ class Workload:
         self.argmax = torch.empty(1, dtype=torch.int32, device=device)
         self.owns_last = rank == world - 1
         self.comm = None
+        self.peers = []          # f1: peers' gathered buffers (NVLink-mapped), at this rank's rows
+        self.peer_maps = []      # (base pointer, offset) to unmap
+        self.barrier_scratch = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def map_peers(self):
+        """Exchange cudaIpcMemHandles of every rank's gathered buffer and map the peers'."""
+        from paper_2504_12526_b200 import _mom
+        handles = [None] * self.world
+        dist.all_gather_object(handles, _mom.ipc_get_handle(self.out))
+        row_bytes = self.d * 2
+        for r in range(self.world):
+            if r != self.rank:
+                ptr = _mom.ipc_open_handle(*handles[r])
+                self.peer_maps.append((ptr, handles[r][1]))
+                self.peers.append(ptr + self.rank * self.S * row_bytes)
+
+    def unmap_peers(self):
+        from paper_2504_12526_b200 import _mom
+        for ptr, off in self.peer_maps:
+            _mom.ipc_close(ptr, off)
+        self.peer_maps, self.peers = [], []
 
     @property
     def shard(self):
@@ -193,13 +216,20 @@ def run_step(wl, compute, copy, launches, x_host=None, h2d=None):
     copy.wait_stream(compute)
     _mom.kv_offload(wl.kv, wl.kv_host, compute, copy)                                   # a9
     wg, wu, wd = wl.w0
-    if x_host is None:
-        _mom.mlp_minseq_fwd(wl.x, wl.x, wg, wu, wd, wl.shard, wl.C, wl.ws, compute)     # a1-a4
-    else:
+    if x_host is not None:
         _mom.mlp_minseq_fwd_from_host(x_host, wl.x, wl.x, wg, wu, wd, wl.shard, wl.C, wl.ws, compute, h2d)
+        if wl.world > 1:
+            _mom.allgather_rows(wl.out, wl.S, wl.comm, wl.rank, wl.world, compute)       # a11 (NCCL)
+    elif wl.world > 1 and wl.peers:
+        # a1-a4 + a11: the phase-B epilogue stores every output row to all peers (f1), then a
+        # 1-element NCCL all-reduce orders everyone's peer stores before the next layer
+        _mom.mlp_minseq_fwd_gather(wl.x, wl.x, wg, wu, wd, wl.shard, wl.peers, wl.C, wl.ws, compute)
+        _mom.nccl_barrier(wl.comm, wl.barrier_scratch, compute)
+    else:
+        _mom.mlp_minseq_fwd(wl.x, wl.x, wg, wu, wd, wl.shard, wl.C, wl.ws, compute)     # a1-a4
+        if wl.world > 1:
+            _mom.allgather_rows(wl.out, wl.S, wl.comm, wl.rank, wl.world, compute)       # a11 (NCCL)
     launches[0] += 2 * wl.M
-    if wl.world > 1:
-        _mom.allgather_rows(wl.out, wl.S, wl.comm, wl.rank, wl.world, compute)           # a11
     if wl.owns_last:
         last = wl.out[wl.world * wl.S - 1]
         wg1, wu1, wd1 = wl.w1
@@ -262,6 +292,8 @@ def run_mine(args):
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         wl.comm = _mom.nccl_comm_init(world, obj[0], rank)
+        if args.gather == "fused":
+            wl.map_peers()
     compute = torch.cuda.Stream(device)
     copy = torch.cuda.Stream(device)
     torch.cuda.synchronize()
@@ -397,6 +429,10 @@ def run_mine(args):
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(wl)
+    if wl.peer_maps:
+        torch.cuda.synchronize()
+        dist.barrier()
+        wl.unmap_peers()
     if wl.comm is not None:
         _mom.nccl_comm_destroy(wl.comm)
     if rank == 0:

@@ -51,12 +51,16 @@ class PrefillStack:
     """MOM prefill of the MLP path over L layers on one GPU (or one token shard of N)."""
 
     def __init__(self, weights, w_head, norm_gain, eps, S_local, minseq_len, kv_shape, device,
-                 world=1, rank=0, comm=None, S_total=None, offload=True, reload=True):
+                 world=1, rank=0, comm=None, S_total=None, offload=True, reload=True, peers=None):
         self.weights = weights            # list of (w_gate, w_up, w_down), layer 0..L-1
         self.L = len(weights)
         self.wh, self.gain, self.eps = w_head, norm_gain, eps
         self.S, self.C = S_local, minseq_len
         self.world, self.rank, self.comm = world, rank, comm
+        # f1: peers' x buffers (NVLink-mapped, offset to this rank's shard rows); the phase-B
+        # epilogue stores every output row there, so no separate all-gather runs
+        self.peers = list(peers or [])
+        self.barrier_scratch = torch.zeros(1, dtype=torch.int32, device=device) if world > 1 else None
         self.S_total = S_total if S_total is not None else S_local * world
         self.device = device
         wg0 = weights[0][0]
@@ -101,10 +105,15 @@ class PrefillStack:
                     on_layer(l, x)
                 wg, wu, wd = self.weights[l]
                 if l < self.L - 1:
-                    _mom.mlp_minseq_fwd(shard, shard, wg, wu, wd, shard, self.C, self.ws, compute)  # a1-a5
+                    if self.world > 1 and self.peers:  # a1-a5 + a11 fused (f1)
+                        _mom.mlp_minseq_fwd_gather(shard, shard, wg, wu, wd, shard, self.peers, self.C, self.ws,
+                                                   compute)
+                        _mom.nccl_barrier(self.comm, self.barrier_scratch, compute)
+                    else:
+                        _mom.mlp_minseq_fwd(shard, shard, wg, wu, wd, shard, self.C, self.ws, compute)  # a1-a5
+                        if self.world > 1:
+                            _mom.allgather_rows(x, self.S, self.comm, self.rank, self.world, compute)  # a11
                     launches += 2 * math.ceil(self.S / self.C)
-                    if self.world > 1:
-                        _mom.allgather_rows(x, self.S, self.comm, self.rank, self.world, compute)  # a11
                 elif self.rank == self.owner:
                     last = x[self.S_total - 1]
                     _mom.mlp_last_token(last, last, wg, wu, wd, self.y, self.ws_last, compute)     # a6
