@@ -9,7 +9,8 @@ Pure control flow around the C-ABI calls (no arithmetic of the method runs here)
   3. non-final layers: mom_mlp_minseq_fwd in place, x <- x + MLP(x), and, when the
      tokens are sharded over N GPUs, mom_allgather_rows rebuilds the [N*S, d] rows;
   4. final layer: mom_mlp_last_token on the last token (P:102-103), mom_lm_head_last (P:105);
-  5. after the head, mom_kv_reload brings every layer's K/V back to the device.
+  5. after the head, mom_kv_reload brings every layer's K/V back to the device, one
+     event per layer (f4: a decode step may start layer l as soon as its K/V is back).
 Token sharding: rank r owns rows [r*S_r, (r+1)*S_r) of N*S_r (padded) rows.
 """
 from __future__ import annotations
@@ -45,13 +46,17 @@ class StackResult:
     kv_host: list = field(default_factory=list)
     kv_dev: list = field(default_factory=list)
     launches: int = 0
+    # f4: one event per layer, recorded on the copy stream when that layer's K/V is back on the
+    # device; a decode step can start layer l after reload_done[l] while layers > l still stream
+    reload_done: list = field(default_factory=list)
 
 
 class PrefillStack:
     """MOM prefill of the MLP path over L layers on one GPU (or one token shard of N)."""
 
     def __init__(self, weights, w_head, norm_gain, eps, S_local, minseq_len, kv_shape, device,
-                 world=1, rank=0, comm=None, S_total=None, offload=True, reload=True, peers=None):
+                 world=1, rank=0, comm=None, S_total=None, offload=True, reload=True, peers=None,
+                 pipelined_reload=False):
         self.weights = weights            # list of (w_gate, w_up, w_down), layer 0..L-1
         self.L = len(weights)
         self.wh, self.gain, self.eps = w_head, norm_gain, eps
@@ -73,6 +78,9 @@ class PrefillStack:
                                    device=device)
         self.ws_head = torch.empty(_mom.lib().mom_lm_head_workspace_bytes(self.V), dtype=torch.uint8, device=device)
         self.offload, self.reload = offload, reload and offload
+        # f4: when True, run() does not join the copy stream after the reload; the caller waits
+        # on StackResult.reload_done[l] per layer (decode of layer l overlaps the H2D of l+1..)
+        self.pipelined_reload = pipelined_reload
         self.kv_shape = kv_shape
         self.kv_ring = [torch.empty(kv_shape, dtype=self.dtype, device=device) for _ in range(2)] if offload else []
         self.kv_host = [torch.empty(kv_shape, dtype=self.dtype, pin_memory=True) for _ in range(self.L)] if offload else []
@@ -120,11 +128,15 @@ class PrefillStack:
                     _mom.lm_head_last(self.y, self.gain, self.eps, self.wh, self.logits, self.argmax,
                                       self.ws_head, compute)                                       # a7-a8
                     launches += 4
+            reload_done = []
             if self.reload:
                 copy.wait_stream(compute)  # Alg. 1: after the head
-                for l in range(self.L):
-                    _mom.kv_reload(self.kv_host[l], self.kv_dev[l], copy)                          # a10
-                compute.wait_stream(copy)
+                for l in range(self.L):     # layer order = decode order (f4: per-layer completion)
+                    ev = torch.cuda.Event()
+                    _mom.kv_reload(self.kv_host[l], self.kv_dev[l], copy, ev)                      # a10
+                    reload_done.append(ev)
+                if not self.pipelined_reload:
+                    compute.wait_stream(copy)
         own = self.rank == self.owner
         return StackResult(self.y if own else None, self.logits if own else None, self.argmax if own else None,
-                           self.kv_host, self.kv_dev, launches)
+                           self.kv_host, self.kv_dev, launches, reload_done)
