@@ -297,6 +297,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     a.rows = (uint32_t)rows; a.d = (uint32_t)hidden; a.I = (uint32_t)intermediate;
     a.h = h; a.out = static_cast<__nv_bfloat16 *>(oi); a.residual = static_cast<const __nv_bfloat16 *>(ri);
     a.cta_group = cta_group; a.policy = policy; a.num_sms = num_sms;
+    a.coalesced_a = static_cast<uint32_t>(env_int("MOM_EPI_A_COALESCED", 1));
     a.ready = reinterpret_cast<uint32_t *>(static_cast<char *>(workspace) + h_bytes(S, intermediate, C, dt));
     a.n_peers = static_cast<uint32_t>(n_peers);  // f1: O_i rows also stored into every peer's gathered buffer
     for (int k = 0; k < n_peers; ++k) a.peer_out[k] = reinterpret_cast<__nv_bfloat16 *>(static_cast<char *>(peers[k]) + off);

@@ -24,6 +24,7 @@ struct TcMlpArgs {
   const __nv_bfloat16 *residual;  // may be null
   const float *row_scale;    // folded RMSNorm 1/rms per row (phase A), or null
   uint32_t *ready;           // fused mode: mlp_tc_ready_counters(rows) zeroed counters
+  uint32_t coalesced_a;      // phase-A epilogue via the smem stage (coalesced H stores)
   uint32_t n_peers;          // f1: number of peer destinations (<= kMaxPeers)
   __nv_bfloat16 *peer_out[kMaxPeers];  // f1: peer gathered buffers at this mini-sequence's rows
   int cta_group;             // 1 or 2

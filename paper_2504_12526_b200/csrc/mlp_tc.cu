@@ -92,6 +92,7 @@ struct Params {
   const __nv_bfloat16 *residual; // phase B residual, may be null
   const float *row_scale;        // phase A: folded-RMSNorm 1/rms per row, or null
   uint32_t *ready;               // MODE_FUSED: per (row block, CTA rank) count of finished phase-A tiles
+  uint32_t coalesced_a;          // phase-A epilogue through the smem stage (128-B row segments)
   uint32_t n_peers;              // f1: extra destinations of the phase-B output rows
   __nv_bfloat16 *peer_out[kMaxPeers];  // f1: peers' gathered buffers, offset like `out`
 };
@@ -211,6 +212,57 @@ __device__ __forceinline__ void epilogue_a(const Params &p, uint32_t taddr, uint
         }
       }
     }
+  }
+}
+
+// Phase A epilogue, coalesced variant: 64 H columns (128 B per row) at a time through the same
+// per-warp 32 x 128 B XOR-swizzled stage as phase B, stored as full 128-B row segments.
+__device__ __forceinline__ void epilogue_a_coalesced(const Params &p, uint32_t taddr, uint32_t row0_warp,
+                                                     uint32_t col0, uint8_t *stage) {
+  const uint32_t lane = ptx::lane_id();
+  const uint32_t row = row0_warp + lane;
+  const uint32_t sbase = ptx::smem_u32(stage);
+  auto sw = [&](uint32_t r, uint32_t v) { return sbase + r * 128 + (((v ^ r) & 7) << 4); };
+  const uint32_t cr = lane >> 3, cv = lane & 7;
+  const float rs = (p.row_scale != nullptr && row < p.rows) ? p.row_scale[row] : 1.0f;
+#pragma unroll 1
+  for (uint32_t c = 0; c < BHALF / 64; ++c) {
+#pragma unroll
+    for (uint32_t half = 0; half < 2; ++half) {  // 32 columns of g and u at a time (register budget)
+      uint32_t g[32], u[32];
+      ptx::tmem_ld_32x32b_x32(taddr + c * 64 + half * 32, g);
+      ptx::tmem_ld_32x32b_x32(taddr + BHALF + c * 64 + half * 32, u);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (uint32_t v = 0; v < 4; ++v) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float g0 = __uint_as_float(g[8 * v + 2 * e]), g1 = __uint_as_float(g[8 * v + 2 * e + 1]);
+          float u0 = __uint_as_float(u[8 * v + 2 * e]), u1 = __uint_as_float(u[8 * v + 2 * e + 1]);
+          if (p.row_scale != nullptr) {
+            g0 *= rs; g1 *= rs; u0 *= rs; u1 *= rs;
+          }
+          w[e] = ptx::pack_bf16x2(silu_mul(g0, u0), silu_mul(g1, u1));
+        }
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sw(lane, half * 4 + v)), "r"(w[0]), "r"(w[1]),
+                     "r"(w[2]), "r"(w[3])
+                     : "memory");
+      }
+    }
+    __syncwarp();
+    const uint32_t ccol = col0 + c * 64;
+#pragma unroll
+    for (uint32_t i = 0; i < 8; ++i) {
+      const uint32_t r = cr + 4 * i, grow = row0_warp + r, gcol = ccol + cv * 8;
+      uint4 v;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                   : "r"(sw(r, cv))
+                   : "memory");
+      if (grow < p.rows && gcol < p.I) *reinterpret_cast<uint4 *>(p.h + size_t(grow) * p.I + gcol) = v;
+    }
+    __syncwarp();
   }
 }
 
@@ -454,7 +506,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t row = tl.m * BM * CG + rank * BM + row_in_tile;
       const bool row_ok = row < p.rows;
       const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * ACC_COLS;
-      if (tl.a)
+      if (tl.a && p.coalesced_a)
+        epilogue_a_coalesced(p, taddr, row - lane, tl.n * BHALF, epi_stage + q * 32 * 128);
+      else if (tl.a)
         epilogue_a(p, taddr, row, row_ok, tl.n * BHALF);
       else
         epilogue_b(p, taddr, row - lane, tl.n * UMMA_N, epi_stage + q * 32 * 128);
@@ -545,6 +599,7 @@ static cudaError_t launch_mode(const TcMlpArgs &a, cudaStream_t stream) {
   p.residual = a.residual;
   p.row_scale = a.row_scale;
   p.ready = a.ready;
+  p.coalesced_a = a.coalesced_a;
   p.n_peers = a.n_peers;
   for (uint32_t k = 0; k < a.n_peers && k < kMaxPeers; ++k) p.peer_out[k] = a.peer_out[k];
   if (a.cta_group == 2) return launch<2, MODE>(maps, p, a.num_sms, stream);
