@@ -25,8 +25,14 @@
  *               per-call state, and never synchronises the host.
  *   Async       Compute calls enqueue kernels on `stream` and return.  Kernel faults surface
  *               at the caller's next synchronisation (as with cuBLAS).
- *   Errors      A non-OK status means NOTHING was enqueued (argument errors are detected
- *               before any launch); mom_last_error() returns a thread-local message.
+ *   Errors      MOM_ERR_INVALID_ARG / _UNSUPPORTED / _WORKSPACE mean NOTHING was enqueued
+ *               (arguments are checked before any launch).  MOM_ERR_CUDA / _NCCL report a failed
+ *               launch or library call; launches of the same call that preceded it (earlier
+ *               mini-sequences) stay enqueued.  mom_last_error() returns a thread-local message.
+ *   Tuning      Environment knobs read per call (defaults are the measured best on B200):
+ *               MOM_CTA_GROUP (2), MOM_GROUP_M_A (16), MOM_GROUP_M_B (8), MOM_TMA_POLICY (0),
+ *               MOM_FUSED (0: two launches per mini-sequence), MOM_EPI_A_COALESCED (1),
+ *               MOM_GEMV_PDL (1).  None changes results: outputs are bitwise identical.
  *   Alignment   Device pointers must be 16-byte aligned and row pitches (hidden*w,
  *               intermediate*w, w = element bytes) multiples of 16 bytes (TMA rule).
  *   Dtypes      MOM_BF16: bf16 storage, fp32 accumulation, fp32 SiLU, one RNE rounding of

@@ -1,0 +1,45 @@
+"""The tuning knobs of include/mom.h change scheduling, caching and store paths only: every setting
+must give the bitwise-identical output (and the same as the default)."""
+from __future__ import annotations
+
+import os
+
+import pytest
+import torch
+
+import synth
+from paper_2504_12526_b200 import _mom
+
+pytestmark = pytest.mark.gpu
+
+KNOBS = [{}, {"MOM_CTA_GROUP": "1"}, {"MOM_GROUP_M_A": "1"}, {"MOM_GROUP_M_A": "5", "MOM_GROUP_M_B": "3"},
+         {"MOM_TMA_POLICY": "1"}, {"MOM_TMA_POLICY": "3"}, {"MOM_TMA_POLICY": "5"}, {"MOM_FUSED": "1"},
+         {"MOM_FUSED": "1", "MOM_GROUP_M_A": "2"}, {"MOM_EPI_A_COALESCED": "0"}]
+ALL = sorted({k for v in KNOBS for k in v})
+
+
+def test_knobs_are_bit_neutral(cuda_device):
+    S, d, I, C = 1500, 512, 1160, 700
+    bf = torch.bfloat16
+    wg, wu, wd = synth.mlp_weights(d, I, 0, cuda_device, bf)
+    x = synth.hidden(S, d, cuda_device, bf)
+    res = synth.hidden(S, d, cuda_device, bf, seed=synth.SEED_X + 1)
+    old = {k: os.environ.get(k) for k in ALL}
+    outs = []
+    try:
+        for knob in KNOBS:
+            for k in ALL:
+                os.environ.pop(k, None)
+            os.environ.update(knob)
+            o = torch.empty_like(x)
+            _mom.mlp_minseq_fwd(x, res, wg, wu, wd, o, C)
+            torch.cuda.synchronize()
+            outs.append(o)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    for knob, o in zip(KNOBS, outs):
+        assert torch.equal(o, outs[0]), knob
