@@ -299,8 +299,23 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     a.cta_group = cta_group; a.policy = policy; a.num_sms = num_sms;
     a.coalesced_a = static_cast<uint32_t>(env_int("MOM_EPI_A_COALESCED", 1));
     a.ready = reinterpret_cast<uint32_t *>(static_cast<char *>(workspace) + h_bytes(S, intermediate, C, dt));
-    a.n_peers = static_cast<uint32_t>(n_peers);  // f1: O_i rows also stored into every peer's gathered buffer
+    // f1: every O_i row must reach every peer.  Rows of mini-sequence i-1 (final once its phase B
+    // completed) are forwarded by warps 2-3 of this mini-sequence's phase-A launch, so the NVLink
+    // traffic overlaps the tensor-core work; only the last mini-sequence's rows are stored to
+    // the peers by the phase-B epilogue that produces them.
+    const bool fwd_mode = env_int("MOM_GATHER_FORWARD", 1) != 0;
+    a.n_peers = (!fwd_mode || i == M - 1) ? static_cast<uint32_t>(n_peers) : 0u;
     for (int k = 0; k < n_peers; ++k) a.peer_out[k] = reinterpret_cast<__nv_bfloat16 *>(static_cast<char *>(peers[k]) + off);
+    a.fwd_src = nullptr;
+    a.fwd_rows = 0;
+    a.n_fwd = 0;
+    if (fwd_mode && n_peers > 0 && i > 0) {
+      const size_t prev = static_cast<size_t>(r0 - C) * hidden * w;
+      a.fwd_src = reinterpret_cast<const __nv_bfloat16 *>(static_cast<const char *>(out) + prev);
+      a.fwd_rows = static_cast<uint32_t>(C);
+      a.n_fwd = static_cast<uint32_t>(n_peers);
+      for (int k = 0; k < n_peers; ++k) a.fwd_dst[k] = reinterpret_cast<__nv_bfloat16 *>(static_cast<char *>(peers[k]) + prev);
+    }
     if (norm_eps) {
       // folded RMSNorm (f3): 1/rms of this mini-sequence's rows, after H_i and the counters
       float *inv = reinterpret_cast<float *>(static_cast<char *>(workspace) +
@@ -328,6 +343,8 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     }
     if (e != cudaSuccess) return cuda_fail(e, "phase A (tcgen05)");
     a.group_m = group_b;
+    a.fwd_src = nullptr;  // forwarding rides on the phase-A launch only
+    a.n_fwd = 0;
     {
       ScopedTiming tm(stream, 1);
       e = mom::launch_mlp_tc(a, 1, stream);  // O_i = R_i + H_i Wd^T, written at rows r0..

@@ -27,6 +27,9 @@ struct TcMlpArgs {
   uint32_t coalesced_a;      // phase-A epilogue via the smem stage (coalesced H stores)
   uint32_t n_peers;          // f1: number of peer destinations (<= kMaxPeers)
   __nv_bfloat16 *peer_out[kMaxPeers];  // f1: peer gathered buffers at this mini-sequence's rows
+  const __nv_bfloat16 *fwd_src;        // f1: previous mini-sequence's output rows to forward (or null)
+  uint32_t fwd_rows, n_fwd;            //     ... its row count and number of destinations
+  __nv_bfloat16 *fwd_dst[kMaxPeers];   //     ... the peers' buffers at those rows
   int cta_group;             // 1 or 2
   uint32_t group_m;          // raster group (0 = default)
   uint32_t policy;           // TMA L2 cache policy variant (0 = default)

@@ -95,6 +95,11 @@ struct Params {
   uint32_t coalesced_a;          // phase-A epilogue through the smem stage (128-B row segments)
   uint32_t n_peers;              // f1: extra destinations of the phase-B output rows
   __nv_bfloat16 *peer_out[kMaxPeers];  // f1: peers' gathered buffers, offset like `out`
+  // f1 forwarding (warps 2-3): rows [0, fwd_rows) of fwd_src (the previous mini-sequence's
+  // finished output) are copied to fwd_dst[0..n_fwd) during this launch
+  const __nv_bfloat16 *fwd_src;
+  uint32_t fwd_rows, n_fwd;
+  __nv_bfloat16 *fwd_dst[kMaxPeers];
 };
 
 struct Tile {
@@ -532,6 +537,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
+  } else if (p.n_fwd > 0) {
+    // ======================= warps 2-3: forward the previous mini-sequence's rows (f1) =========
+    // Its output rows are final (the previous launch completed); copy this CTA's share of them
+    // to every peer while the tensor cores work on this mini-sequence.  64 threads per CTA,
+    // 16-B units, 4 independent loads in flight per thread.
+    const uint32_t tid = threadIdx.x - 64;  // 0..63
+    const size_t units = static_cast<size_t>(p.fwd_rows) * (p.d / 8);
+    const size_t per_cta = (units + gridDim.x - 1) / gridDim.x;
+    const size_t u0 = static_cast<size_t>(blockIdx.x) * per_cta;
+    const size_t u1 = u0 + per_cta < units ? u0 + per_cta : units;
+    const uint4 *src = reinterpret_cast<const uint4 *>(p.fwd_src);
+    for (size_t u = u0 + tid; u < u1; u += 4 * 64) {
+      uint4 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (u + j * 64 < u1) v[j] = src[u + j * 64];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (u + j * 64 < u1)
+          for (uint32_t k = 0; k < p.n_fwd; ++k) reinterpret_cast<uint4 *>(p.fwd_dst[k])[u + j * 64] = v[j];
+    }
   }
 
   ptx::tc_fence_before();
@@ -600,6 +626,10 @@ static cudaError_t launch_mode(const TcMlpArgs &a, cudaStream_t stream) {
   p.row_scale = a.row_scale;
   p.ready = a.ready;
   p.coalesced_a = a.coalesced_a;
+  p.fwd_src = a.fwd_src;
+  p.fwd_rows = a.fwd_rows;
+  p.n_fwd = a.fwd_src ? a.n_fwd : 0;
+  for (uint32_t k = 0; k < p.n_fwd && k < kMaxPeers; ++k) p.fwd_dst[k] = a.fwd_dst[k];
   p.n_peers = a.n_peers;
   for (uint32_t k = 0; k < a.n_peers && k < kMaxPeers; ++k) p.peer_out[k] = a.peer_out[k];
   if (a.cta_group == 2) return launch<2, MODE>(maps, p, a.num_sms, stream);

@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(autouse=True)
 def _env():
-    keys = ("MOM_FUSED", "MOM_CTA_GROUP")
+    keys = ("MOM_FUSED", "MOM_CTA_GROUP", "MOM_GATHER_FORWARD")
     old = {k: os.environ.get(k) for k in keys}
     yield
     for k, v in old.items():
@@ -31,9 +31,11 @@ def _env():
             os.environ[k] = v
 
 
-@pytest.mark.parametrize("fused,cg", [("0", "2"), ("1", "2"), ("0", "1")])
-def test_gather_into_local_peer_buffers(cuda_device, fused, cg):
-    os.environ["MOM_FUSED"], os.environ["MOM_CTA_GROUP"] = fused, cg
+@pytest.mark.parametrize("fused,cg,fwd", [("0", "2", "1"), ("0", "2", "0"), ("1", "2", "1"), ("0", "1", "1")])
+def test_gather_into_local_peer_buffers(cuda_device, fused, cg, fwd):
+    """fwd=1: rows of mini-sequence i-1 are forwarded by warps 2-3 during mini-sequence i's phase A,
+    the last mini-sequence's rows by its phase-B epilogue; fwd=0: every epilogue stores to peers."""
+    os.environ["MOM_FUSED"], os.environ["MOM_CTA_GROUP"], os.environ["MOM_GATHER_FORWARD"] = fused, cg, fwd
     S, d, I, C, world, rank = 700, 512, 1024, 256, 4, 2
     bf = torch.bfloat16
     wg, wu, wd = synth.mlp_weights(d, I, 0, cuda_device, bf)
