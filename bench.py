@@ -66,32 +66,37 @@ def parse_args():
 
 
 # ----------------------------------------------------------------------------- distributed
+# Test mode for the N > 1 code path on a one-GPU box: every rank on cuda:0, gloo instead of NCCL,
+# host barriers instead of mom_nccl_barrier, no e2e leg.  Never used for a reported number.
+SHARED_GPU = os.environ.get("MOM_BENCH_SHARED_GPU") == "1"
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if SHARED_GPU else int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 and not dist.is_initialized():
-        backend = "nccl" if torch.cuda.is_available() and args.impl == "mine" else "gloo"
+        backend = "nccl" if torch.cuda.is_available() and args.impl == "mine" and not SHARED_GPU else "gloo"
         if backend == "nccl":
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
     return world, rank, local
 
 
-def max_over_ranks(x: float, world: int, device) -> float:
+def _reduce(x: float, world: int, device, op) -> float:
     if world == 1:
         return x
-    t = torch.tensor([x], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARED_GPU else device)
+    dist.all_reduce(t, op=op)
     return float(t.item())
+
+
+def max_over_ranks(x: float, world: int, device) -> float:
+    return _reduce(x, world, device, dist.ReduceOp.MAX)
 
 
 def sum_over_ranks(x: float, world: int, device) -> float:
-    if world == 1:
-        return x
-    t = torch.tensor([x], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    return _reduce(x, world, device, dist.ReduceOp.SUM)
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -225,7 +230,11 @@ def run_step(wl, compute, copy, launches, x_host=None, h2d=None):
         # a1-a4 + a11: the phase-B epilogue stores every output row to all peers (f1), then a
         # 1-element NCCL all-reduce orders everyone's peer stores before the next layer
         _mom.mlp_minseq_fwd_gather(wl.x, wl.x, wg, wu, wd, wl.shard, wl.peers, wl.C, wl.ws, compute)
-        _mom.nccl_barrier(wl.comm, wl.barrier_scratch, compute)
+        if wl.comm is not None:
+            _mom.nccl_barrier(wl.comm, wl.barrier_scratch, compute)
+        else:  # SHARED_GPU test mode: host barrier
+            compute.synchronize()
+            dist.barrier()
     else:
         _mom.mlp_minseq_fwd(wl.x, wl.x, wg, wu, wd, wl.shard, wl.C, wl.ws, compute)     # a1-a4
         if wl.world > 1:
@@ -290,10 +299,13 @@ def run_mine(args):
     peaks, peaks_src = load_peaks()
     wl = Workload(cfg, rank, world, device)
     if world > 1:
-        uid = _mom.nccl_get_unique_id() if rank == 0 else bytes(128)
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        wl.comm = _mom.nccl_comm_init(world, obj[0], rank)
+        if not SHARED_GPU:
+            uid = _mom.nccl_get_unique_id() if rank == 0 else bytes(128)
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0)
+            wl.comm = _mom.nccl_comm_init(world, obj[0], rank)
+        else:
+            args.no_e2e = True
         if args.gather == "fused":
             wl.map_peers()
     compute = torch.cuda.Stream(device)
