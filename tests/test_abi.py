@@ -103,3 +103,34 @@ def test_invalid_arguments_rejected_before_launch(lib):
     assert lib.mom_kv_reload(16, None, 10, None, None) == E
     assert lib.mom_allgather_rows(16, 4, 8, 0, None, 0, 2, None) == E
     assert lib.mom_nccl_comm_init(None, 2, None, 0) == E
+
+
+def test_new_entry_points_reject_bad_arguments(lib):
+    """f1-f3 / e2e entries: argument errors come back before any CUDA call (CPU box)."""
+    E, U = _mom.MOM_ERR_INVALID_ARG, _mom.MOM_ERR_UNSUPPORTED
+    P = ctypes.c_void_p
+    peers = (P * 1)(None)
+    # gather: null peer pointer, too many peers
+    assert lib.mom_mlp_minseq_fwd_gather(16, None, 32, 48, 64, 80, peers, 1, 4, 8, 16, 2, 0, 96, 1 << 20, None) == E
+    assert lib.mom_mlp_minseq_fwd_gather(16, None, 32, 48, 64, 80, peers, 8, 4, 8, 16, 2, 0, 96, 1 << 20, None) == E
+    # from_host: null host pointer
+    assert lib.mom_mlp_minseq_fwd_from_host(None, 16, None, 32, 48, 64, 80, 4, 8, 16, 2, 0, 96, 1 << 20, None,
+                                            None) == E
+    # folded norm: fp32 unsupported, bad eps, misaligned
+    assert lib.mom_fold_norm_gain(16, 32, 48, 4, 8, _mom.MOM_F32, None) == U
+    assert lib.mom_fold_norm_gain(16, 32, 48, 4, 6, _mom.MOM_BF16, None) == E
+    assert lib.mom_mlp_minseq_rmsnorm_fwd(16, 32, 48, 64, 80, 4, 8, 16, 2, -1.0, 0, 96, 1 << 20, None) == E
+    assert lib.mom_mlp_minseq_rmsnorm_fwd(16, 32, 48, 64, 80, 4, 8, 16, 2, 1e-5, _mom.MOM_F32, 96, 1 << 20, None) == U
+    # vocab shard / argmax all-reduce / barrier / IPC
+    assert lib.mom_lm_head_shard(16, None, 0.0, 32, -1, 10, None, 48, 8, 0, 64, 1 << 16, None) == E
+    assert lib.mom_lm_head_shard(16, None, 0.0, 32, 0, 10, None, 44, 8, 0, 64, 1 << 16, None) == E  # key align
+    assert lib.mom_argmax_allreduce(None, 16, None, None) == E
+    assert lib.mom_nccl_barrier(None, 16, None) == E
+    assert lib.mom_ipc_get_handle(None, None, None) == E
+    assert lib.mom_ipc_open_handle(None, 0, None) == E
+    assert lib.mom_ipc_close(None, 0) == E
+    assert lib.mom_set_timing_events(16, None, 4, None) == E
+    assert lib.mom_set_timing_events(None, None, 0, None) == _mom.MOM_OK  # disabling is always fine
+    # rmsnorm workspace = plain workspace + C fp32 scales (rounded)
+    base = lib.mom_mlp_minseq_workspace_bytes(4096, 512, 1024, 512, _mom.MOM_BF16)
+    assert lib.mom_mlp_minseq_rmsnorm_workspace_bytes(4096, 512, 1024, 512, _mom.MOM_BF16) == base + 512 * 4
