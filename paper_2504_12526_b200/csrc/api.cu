@@ -84,12 +84,13 @@ EncodeFn encode_fn() {
 }
 
 // 2D bf16 row-major [rows, cols] tensor, box = 64 columns (128 B, one 128-B swizzle span) x 128 rows.
-mom_status_t make_tmap(CUtensorMap *m, const void *base, uint64_t rows, uint64_t cols, const char *what) {
+mom_status_t make_tmap(CUtensorMap *m, const void *base, uint64_t rows, uint64_t cols, const char *what,
+                       uint32_t box_rows = 128) {
   EncodeFn enc = encode_fn();
   if (!enc) return fail(MOM_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -144,6 +145,27 @@ size_t h_bytes(int64_t S, int64_t I, int64_t C, mom_dtype_t dt) {
 int env_int(const char *name, int dflt) {
   const char *v = getenv(name);
   return (v && *v) ? atoi(v) : dflt;
+}
+
+// Phase-B tile width: the persistent grid runs ceil(tiles / clusters) waves and a tile's time is
+// proportional to its width, so pick the width (multiple of 32, <= 256) minimising
+// waves * width -- e.g. hidden 3584: 14 tiles of 256 -> 7 waves, 16 tiles of 224 -> 7 shorter waves.
+uint32_t pick_phase_b_width(int64_t rows, int64_t hidden, int cta_group, int num_sms) {
+  const int forced = env_int("MOM_NB_B", 0);
+  if (forced >= 32 && forced <= 256 && forced % 32 == 0) return static_cast<uint32_t>(forced);
+  const int64_t m_tiles = (rows + 128 * cta_group - 1) / (128 * cta_group);
+  const int64_t clusters = num_sms / cta_group > 0 ? num_sms / cta_group : 1;
+  uint32_t best = 256;
+  int64_t best_cost = -1;
+  for (uint32_t nb = 256; nb >= 128; nb -= 32) {
+    const int64_t tiles = m_tiles * ((hidden + nb - 1) / nb);
+    const int64_t cost = ((tiles + clusters - 1) / clusters) * nb;
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = nb;
+    }
+  }
+  return best;
 }
 
 }  // namespace
@@ -246,8 +268,8 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
   if (dt == MOM_BF16) {
     if ((st = make_tmap(&tm_wg, w_gate, intermediate, hidden, "w_gate")) != MOM_OK) return st;
     if ((st = make_tmap(&tm_wu, w_up, intermediate, hidden, "w_up")) != MOM_OK) return st;
-    if ((st = make_tmap(&tm_wd, w_down, hidden, intermediate, "w_down")) != MOM_OK) return st;
   }
+  uint32_t wd_box = 0;  // W_down map is (re)encoded when the phase-B tile width changes
   for (int64_t i = 0; i < M; ++i) {  // Alg. 1: for i = 1..M (sequential on `stream`)
     const int64_t r0 = i * C;
     const int64_t rows = (r0 + C < S) ? C : S - r0;
@@ -297,6 +319,11 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     a.rows = (uint32_t)rows; a.d = (uint32_t)hidden; a.I = (uint32_t)intermediate;
     a.h = h; a.out = static_cast<__nv_bfloat16 *>(oi); a.residual = static_cast<const __nv_bfloat16 *>(ri);
     a.cta_group = cta_group; a.policy = policy; a.num_sms = num_sms;
+    a.nb = pick_phase_b_width(rows, hidden, cta_group, num_sms);
+    if (a.nb != wd_box) {  // B halves of phase B are nb/2 rows of W_down per CTA
+      if ((st = make_tmap(&tm_wd, w_down, hidden, intermediate, "w_down", a.nb / 2)) != MOM_OK) return st;
+      wd_box = a.nb;
+    }
     a.coalesced_a = static_cast<uint32_t>(env_int("MOM_EPI_A_COALESCED", 1));
     a.ready = reinterpret_cast<uint32_t *>(static_cast<char *>(workspace) + h_bytes(S, intermediate, C, dt));
     // f1: every O_i row must reach every peer.  Rows of mini-sequence i-1 (final once its phase B

@@ -30,6 +30,7 @@ struct TcMlpArgs {
   const __nv_bfloat16 *fwd_src;        // f1: previous mini-sequence's output rows to forward (or null)
   uint32_t fwd_rows, n_fwd;            //     ... its row count and number of destinations
   __nv_bfloat16 *fwd_dst[kMaxPeers];   //     ... the peers' buffers at those rows
+  uint32_t nb;               // phase-B tile width (multiple of 32, <= 256; 0 = 256); W_down map box = nb/2 rows
   int cta_group;             // 1 or 2
   uint32_t group_m;          // raster group (0 = default)
   uint32_t policy;           // TMA L2 cache policy variant (0 = default)

@@ -84,7 +84,8 @@ struct Params {
   uint32_t rows;         // valid rows of this mini-sequence (C_i)
   uint32_t d, I;         // hidden, intermediate
   uint32_t m_tiles;      // ceil(rows / (BM*CG))
-  uint32_t nA, nB;       // N tiles of phase A (I/128) and phase B (d/256)
+  uint32_t nA, nB;       // N tiles of phase A (I/128) and phase B (d/nb)
+  uint32_t nb;           // phase-B tile width (UMMA N, multiple of 32, <= 256), chosen for wave quantisation
   uint32_t group_m;      // raster: row blocks per group (N iterates inside a group)
   uint32_t policy;       // TMA L2 policy: 0 reuse-aware (default), 1 all evict_normal, 2 A evict_first
   __nv_bfloat16 *h;              // phase A output H_i [rows, I]
@@ -286,7 +287,8 @@ __device__ __forceinline__ void epilogue_b(const Params &p, uint32_t taddr, uint
   auto sw = [&](uint32_t r, uint32_t v) { return sbase + r * 128 + (((v ^ r) & 7) << 4); };
   const uint32_t cr = lane >> 3, cv = lane & 7;  // coalesced mapping: lane -> (row cr + 4i, unit cv)
 #pragma unroll 1
-  for (uint32_t c = 0; c < UMMA_N / 64; ++c) {
+  const uint32_t cend = col0 + p.nb < p.d ? col0 + p.nb : p.d;  // end of this tile's valid columns
+  for (uint32_t c = 0; c < (p.nb + 63) / 64; ++c) {
     const uint32_t ccol = col0 + c * 64;  // first column of this chunk
     uint32_t a[64];
     ptx::tmem_ld_32x32b_x32(taddr + c * 64, *reinterpret_cast<uint32_t(*)[32]>(a));
@@ -297,7 +299,7 @@ __device__ __forceinline__ void epilogue_b(const Params &p, uint32_t taddr, uint
       for (uint32_t i = 0; i < 8; ++i) {
         const uint32_t r = cr + 4 * i, grow = row0_warp + r, gcol = ccol + cv * 8;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (grow < p.rows && gcol < p.d) v = *reinterpret_cast<const uint4 *>(p.residual + size_t(grow) * p.d + gcol);
+        if (grow < p.rows && gcol < cend) v = *reinterpret_cast<const uint4 *>(p.residual + size_t(grow) * p.d + gcol);
         asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sw(r, cv)), "r"(v.x), "r"(v.y), "r"(v.z),
                      "r"(v.w)
                      : "memory");
@@ -340,7 +342,7 @@ __device__ __forceinline__ void epilogue_b(const Params &p, uint32_t taddr, uint
                    : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                    : "r"(sw(r, cv))
                    : "memory");
-      if (grow < p.rows && gcol < p.d) {
+      if (grow < p.rows && gcol < cend) {
         const size_t off = size_t(grow) * p.d + gcol;
         *reinterpret_cast<uint4 *>(p.out + off) = v;
         for (uint32_t k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint4 *>(p.peer_out[k] + off) = v;
@@ -438,8 +440,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           default: pol_a = tl.a ? pol_keep : pol_norm; pol_b = tl.a ? pol_norm : pol_keep; break;
         }
         const int32_t a_row = static_cast<int32_t>(tl.m * BM * CG + rank * BM);
-        const int32_t b_row0 = static_cast<int32_t>(tl.a ? tl.n * BHALF : tl.n * UMMA_N);
-        const int32_t b_off1 = tl.a ? 0 : static_cast<int32_t>(BHALF);  // row offset of B half 1
+        const int32_t b_row0 = static_cast<int32_t>(tl.a ? tl.n * BHALF : tl.n * p.nb);
+        const int32_t b_off1 = tl.a ? 0 : static_cast<int32_t>(p.nb / 2);  // row offset of B half 1
+        // bytes landing per stage: phase B's B halves are nb/2 rows (nb < 256 for some shapes)
+        const uint32_t bhalf_bytes = tl.a ? BHALF_BYTES : (p.nb / 2) * BK * 2;
+        const uint32_t tx_bytes = (A_BYTES + (CG == 1 ? 2 : 1) * bhalf_bytes) * CG;
         const uint32_t num_kb = tl.a ? kbA : kbB;
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -447,11 +452,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t sa = ptx::smem_u32(smem_a + stage * A_BYTES);
           const uint32_t sb = ptx::smem_u32(smem_b + stage * C::B_BYTES);
           const uint32_t fbar = full_leader0 + stage * 8;
-          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], C::TX_BYTES);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], tx_bytes);
           if constexpr (CG == 1) {
             ptx::tma_load_2d(ta, sa, fbar, kc, a_row, pol_a);
             ptx::tma_load_2d(tb0, sb, fbar, kc, b_row0, pol_b);
-            ptx::tma_load_2d(tb1, sb + BHALF_BYTES, fbar, kc, b_row0 + b_off1, pol_b);
+            ptx::tma_load_2d(tb1, sb + bhalf_bytes, fbar, kc, b_row0 + b_off1, pol_b);
           } else {
             ptx::tma_load_2d_cg2(ta, sa, fbar, kc, a_row, pol_a);
             if (rank == 0)
@@ -472,12 +477,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 1) {
     // ======================= MMA issuer (leader CTA, one thread) =======================
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM * CG, UMMA_N);
+      constexpr uint32_t idesc_a = ptx::idesc_bf16_f32(BM * CG, UMMA_N);
+      const uint32_t idesc_b = ptx::idesc_bf16_f32(BM * CG, p.nb);
       uint32_t stage = 0, phase = 0;
       uint32_t acc = 0, acc_phase = 0;
       for (uint32_t t = cluster_id; t < num_tiles; t += num_clusters) {
         const Tile tl = decode_tile<MODE>(t, p);
         const uint32_t num_kb = tl.a ? kbA : kbB;
+        const uint32_t idesc = tl.a ? idesc_a : idesc_b;
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * ACC_COLS;
@@ -516,7 +523,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       else if (tl.a)
         epilogue_a(p, taddr, row, row_ok, tl.n * BHALF);
       else
-        epilogue_b(p, taddr, row - lane, tl.n * UMMA_N, epi_stage + q * 32 * 128);
+        epilogue_b(p, taddr, row - lane, tl.n * p.nb, epi_stage + q * 32 * 128);
       // release the accumulator to the MMA issuer
       ptx::tc_fence_before();
       __syncwarp();
@@ -614,7 +621,8 @@ static cudaError_t launch_mode(const TcMlpArgs &a, cudaStream_t stream) {
   p.I = a.I;
   p.m_tiles = (a.rows + BM * a.cta_group - 1) / (BM * a.cta_group);
   p.nA = (a.I + BHALF - 1) / BHALF;
-  p.nB = (a.d + UMMA_N - 1) / UMMA_N;
+  p.nb = a.nb ? a.nb : UMMA_N;
+  p.nB = (a.d + p.nb - 1) / p.nb;
   // raster groups (energy sweep r1): 16 row blocks for phase A (X rows stay in L2), 8 for B
   uint32_t g = a.group_m ? a.group_m : (MODE == MODE_B ? 8 : 16);
   if (g > p.m_tiles) g = p.m_tiles;
