@@ -155,13 +155,18 @@ uint32_t pick_phase_b_width(int64_t rows, int64_t hidden, int cta_group, int num
   if (forced >= 32 && forced <= 256 && forced % 32 == 0) return static_cast<uint32_t>(forced);
   const int64_t m_tiles = (rows + 128 * cta_group - 1) / (128 * cta_group);
   const int64_t clusters = num_sms / cta_group > 0 ? num_sms / cta_group : 1;
+  auto cost = [&](uint32_t nb) { return ((m_tiles * ((hidden + nb - 1) / nb) + clusters - 1) / clusters) * nb; };
+  // Narrower tiles cost energy per FLOP (more operand traffic), so only take one that divides
+  // hidden exactly and beats 256 by > 5 % in the wave model (measured: +1.2 % at hidden 3584,
+  // a loss at hidden 5120 with a partial last tile).
+  const int64_t base = cost(256);
   uint32_t best = 256;
-  int64_t best_cost = -1;
-  for (uint32_t nb = 256; nb >= 128; nb -= 32) {
-    const int64_t tiles = m_tiles * ((hidden + nb - 1) / nb);
-    const int64_t cost = ((tiles + clusters - 1) / clusters) * nb;
-    if (best_cost < 0 || cost < best_cost) {
-      best_cost = cost;
+  int64_t best_cost = base;
+  for (uint32_t nb = 224; nb >= 128; nb -= 32) {
+    if (hidden % nb) continue;
+    const int64_t c = cost(nb);
+    if (c * 100 < base * 95 && c < best_cost) {
+      best_cost = c;
       best = nb;
     }
   }
