@@ -286,8 +286,8 @@ __device__ __forceinline__ void epilogue_b(const Params &p, uint32_t taddr, uint
   // 16-B unit v of row r of the stage lives at byte r*128 + ((v ^ r) & 7) * 16
   auto sw = [&](uint32_t r, uint32_t v) { return sbase + r * 128 + (((v ^ r) & 7) << 4); };
   const uint32_t cr = lane >> 3, cv = lane & 7;  // coalesced mapping: lane -> (row cr + 4i, unit cv)
-#pragma unroll 1
   const uint32_t cend = col0 + p.nb < p.d ? col0 + p.nb : p.d;  // end of this tile's valid columns
+#pragma unroll 1
   for (uint32_t c = 0; c < (p.nb + 63) / 64; ++c) {
     const uint32_t ccol = col0 + c * 64;  // first column of this chunk
     uint32_t a[64];
