@@ -540,8 +540,7 @@ mom_status_t mom_mlp_minseq_rmsnorm_fwd(const void *x, const void *w_gate_folded
 
 size_t mom_mlp_last_token_workspace_bytes(int64_t intermediate) {
   if (intermediate < 1) return 0;
-  // h (fp32) + 256 B for the cooperative kernel's grid-barrier counter
-  return (((static_cast<size_t>(intermediate) * 4) + 255) & ~static_cast<size_t>(255)) + 256;
+  return ((static_cast<size_t>(intermediate) * 4) + 255) & ~static_cast<size_t>(255);  // h, fp32
 }
 
 mom_status_t mom_mlp_last_token(const void *x_last, const void *residual_last, const void *w_gate,

@@ -385,151 +385,10 @@ static cudaError_t set_smem(K kfn, size_t bytes) {
 
 }  // namespace gemv
 
-namespace gemv {
-
-// Both GEMVs of the last-token MLP in ONE cooperative launch: phase 1 streams W_gate/W_up, a
-// grid-wide barrier, phase 2 streams W_down -- one ramp-up instead of two, no launch gap.
-// Block b owns a contiguous row range of each phase; its 8 warps split every row's K range
-// (vector v of a row goes to warp (v / 32) % 8), partial sums meet in shared memory.  Rows are
-// processed RB at a time so each lane keeps 2*RB*(nvec/256) 16-B loads in flight.
-template <bool BF16, int RB>
-__device__ __forceinline__ void rows_dot_block(const char *w0, const char *w1, size_t pitch, int r0, int nrows,
-                                               const float *vec, int n, float (*red)[2][WARPS], float *res0,
-                                               float *res1) {
-  constexpr int EPV = BF16 ? 8 : 4;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nvec = n / EPV;
-  for (int rb = 0; rb < nrows; rb += RB) {
-    float a0[RB], a1[RB];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) a0[r] = a1[r] = 0.f;
-    for (int v0 = wid * 32; v0 < nvec; v0 += WARPS * 32 * 2) {  // two vectors per lane per round
-      uint4 q0[RB][2], q1[RB][2];
-#pragma unroll
-      for (int r = 0; r < RB; ++r)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int v = v0 + j * WARPS * 32 + lane;
-          const bool ok = rb + r < nrows && v < nvec;
-          const size_t row = static_cast<size_t>(r0 + rb + r);
-          q0[r][j] = ok ? ld_stream(reinterpret_cast<const uint4 *>(w0 + row * pitch) + v) : make_uint4(0, 0, 0, 0);
-          if (w1) q1[r][j] = ok ? ld_stream(reinterpret_cast<const uint4 *>(w1 + row * pitch) + v) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int v = v0 + j * WARPS * 32 + lane;
-        if (v >= nvec) continue;
-        const float *xv = vec + v * EPV;
-#pragma unroll
-        for (int r = 0; r < RB; ++r) {
-          a0[r] += BF16 ? dot8_bf16(q0[r][j], xv) : dot4_f32(q0[r][j], xv);
-          if (w1) a1[r] += BF16 ? dot8_bf16(q1[r][j], xv) : dot4_f32(q1[r][j], xv);
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      a0[r] = warp_sum(a0[r]);
-      if (w1) a1[r] = warp_sum(a1[r]);
-      if (lane == 0) {
-        red[r][0][wid] = a0[r];
-        red[r][1][wid] = a1[r];
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x < RB && rb + threadIdx.x < nrows) {
-      float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-      for (int w = 0; w < WARPS; ++w) {
-        s0 += red[threadIdx.x][0][w];
-        s1 += red[threadIdx.x][1][w];
-      }
-      res0[rb + threadIdx.x] = s0;
-      res1[rb + threadIdx.x] = s1;
-    }
-    __syncthreads();
-  }
-}
-
-template <bool BF16>
-__global__ void __launch_bounds__(THREADS) last_token_coop(const void *__restrict__ x, const void *__restrict__ residual,
-                                                           const void *__restrict__ wg, const void *__restrict__ wu,
-                                                           const void *__restrict__ wd, void *__restrict__ out,
-                                                           float *__restrict__ h, unsigned int *__restrict__ bar,
-                                                           int d, int I) {
-  extern __shared__ float vec[];  // phase 1: x (d floats); phase 2: h (I floats)
-  __shared__ float red[4][2][WARPS];
-  __shared__ float g_s[4], u_s[4];
-  const size_t es = BF16 ? 2 : 4;
-  // ---- phase 1: h[j] = Swish(Wg[j] . x) * (Wu[j] . x) for this block's rows
-  stage_vec<BF16>(x, vec, d);
-  __syncthreads();
-  {
-    const int per = (I + gridDim.x - 1) / gridDim.x;
-    const int r0 = blockIdx.x * per, r1 = r0 + per < I ? r0 + per : I;
-    for (int rb = r0; rb < r1; rb += 4) {
-      const int nr = r1 - rb < 4 ? r1 - rb : 4;
-      rows_dot_block<BF16, 4>(static_cast<const char *>(wg), static_cast<const char *>(wu), d * es, rb, nr, vec, d,
-                              red, g_s, u_s);
-      if (threadIdx.x < nr) {
-        const float g = g_s[threadIdx.x], u = u_s[threadIdx.x];
-        h[rb + threadIdx.x] = g / (1.0f + __expf(-g)) * u;
-      }
-    }
-  }
-  // ---- grid-wide barrier (cooperative launch: all blocks co-resident); the counter is zeroed
-  // by the launcher; __threadfence publishes h and invalidates this SM's L1 for the reads below
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
-    while (*reinterpret_cast<volatile unsigned int *>(bar) < gridDim.x) __nanosleep(64);
-    __threadfence();
-  }
-  __syncthreads();
-  // ---- phase 2: out[c] = residual[c] + Wd[c] . h
-  for (int j = threadIdx.x; j < I; j += THREADS) vec[j] = __ldcg(h + j);
-  __syncthreads();
-  {
-    const int per = (d + gridDim.x - 1) / gridDim.x;
-    const int r0 = blockIdx.x * per, r1 = r0 + per < d ? r0 + per : d;
-    for (int rb = r0; rb < r1; rb += 4) {
-      const int nr = r1 - rb < 4 ? r1 - rb : 4;
-      rows_dot_block<BF16, 4>(static_cast<const char *>(wd), nullptr, I * es, rb, nr, vec, I, red, g_s, u_s);
-      if (threadIdx.x < nr) {
-        const int c = rb + threadIdx.x;
-        const float r = residual ? load_elem<BF16>(residual, c) : 0.f;
-        store_elem<BF16>(out, c, r + g_s[threadIdx.x]);
-      }
-    }
-  }
-}
-
-}  // namespace gemv
-
 cudaError_t launch_last_token_mlp(const void *x, const void *residual, const void *wg, const void *wu,
                                   const void *wd, void *out, float *h_ws, int d, int I, bool is_bf16, int num_sms,
                                   cudaStream_t stream) {
   using namespace gemv;
-  if (env_or("MOM_GEMV_COOP", 1)) {
-    // one cooperative launch; the grid barrier counter lives after h in the workspace
-    unsigned int *bar = reinterpret_cast<unsigned int *>(h_ws + ((I + 63) / 64) * 64);
-    const size_t smem = static_cast<size_t>(d > I ? d : I) * sizeof(float);
-    void *kfn = is_bf16 ? reinterpret_cast<void *>(last_token_coop<true>) : reinterpret_cast<void *>(last_token_coop<false>);
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, THREADS, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    int blocks = num_sms * per_sm;
-    // whole rows per block: no more blocks than rows of the larger phase
-    if (blocks > I) blocks = I;
-    if ((e = cudaMemsetAsync(bar, 0, sizeof(unsigned int), stream)) != cudaSuccess) return e;
-    void *args[] = {const_cast<void **>(&x), const_cast<void **>(&residual), const_cast<void **>(&wg),
-                    const_cast<void **>(&wu), const_cast<void **>(&wd), &out, &h_ws, &bar, &d, &I};
-    return cudaLaunchCooperativeKernel(kfn, dim3(blocks), dim3(THREADS), args, smem, stream);
-  }
   const size_t smem1 = static_cast<size_t>(d) * sizeof(float);
   // Balanced single-wave grids: r = ceil(rows / resident warps) rows per warp, and just enough
   // warps that every warp gets r rows (or r - 1 for the last ones) -- no half-empty second round.
