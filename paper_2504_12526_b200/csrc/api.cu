@@ -194,7 +194,8 @@ mom_status_t mom_set_timing_events(mom_event_t *events, int32_t *kinds, int64_t 
 }
 
 const char *mom_version(void) {
-  return "libmom 0.1 sm_100a: tcgen05 dual-B GEMM (cta_group 1|2), SIMT f32, GEMV, KV copy, NCCL allgather";
+  return "libmom 0.2 sm_100a: tcgen05 2-CTA SwiGLU MLP (phase A/B, fused option), fused all-gather stores, "
+         "folded RMSNorm, SIMT f32, PDL GEMVs + argmax, vocab-sharded head, KV copies, NCCL";
 }
 
 int64_t mom_plan_minseq(int64_t S, int64_t C, int64_t *starts, int64_t *lens, int64_t cap) {
