@@ -304,6 +304,22 @@ def measure_peak_activation(wl, C):
     return torch.cuda.max_memory_allocated() - base
 
 
+def measure_eager_unchunked(wl):
+    """Peak extra device bytes of a plain PyTorch-eager SwiGLU over all S rows (not our path: the
+    memory comparator of SURVEY §8(d)(iii); its output is discarded)."""
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    wg, wu, wd = wl.w0
+    with torch.no_grad():
+        y = wl.x + torch.nn.functional.linear(
+            torch.nn.functional.silu(torch.nn.functional.linear(wl.x, wg)) * torch.nn.functional.linear(wl.x, wu), wd)
+    torch.cuda.synchronize()
+    peak = torch.cuda.max_memory_allocated() - base
+    del y
+    return peak
+
+
 def cpu_baseline(wl, target_s: float = 15.0):
     """The oracle as it stands on a bounded sample of the workload (rows of the MLP layer)."""
     import oracle
@@ -321,7 +337,13 @@ def cpu_baseline(wl, target_s: float = 15.0):
     t0 = time.perf_counter()
     oracle.mlp_rows(x, x, wg, wu, wd, rows2, nthreads=threads)
     dt = time.perf_counter() - t0
+    # the same oracle on one host thread, a short sample
+    rows1 = rows2[: max(1, min(len(rows2), int(3.0 * len(rows2) / max(dt, 1e-3) / threads)))]
+    t0 = time.perf_counter()
+    oracle.mlp_rows(x, x, wg, wu, wd, rows1, nthreads=1)
+    dt1 = time.perf_counter() - t0
     return {"value": len(rows2) / dt, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+            "value_1_thread": len(rows1) / dt1,
             "sample": f"{len(rows2)} sampled rows of the layer-0 MLP (config 2 shapes, float64 C oracle, "
                       f"{dt:.1f} s); the last-token path is amortised over S and excluded"}
 
@@ -451,6 +473,7 @@ def run_mine(args):
                      "achieved": ach_a, "peak": peak, "unit": "TFLOP/s", "frac": ach_a / peak,
                      "traffic": traffic, "peak_source": peak_src,
                      "frac_of_burst_peak": ach_a / burst, "frac_of_sustained_peak": ach_a / sustained,
+                     "frac_of_spec_dense_bf16": ach_a / 2250.0,
                      "flop_per_launch": flops_a},
         "kernels": kernels,
         "mlp_only": {"ms": mlp_ms, "tokens_per_s": S / (mlp_ms * 1e-3),
@@ -485,6 +508,10 @@ def run_mine(args):
         result["peak_activation_gb"] = pa / 1e9
         result["peak_activation_unchunked_eq1_gb"] = S * I * 2 / 1e9
         result["activation_reduction_x"] = (S * I * 2) / max(pa, 1)
+        # the comparators of SURVEY §8(d): the same library at C = S (M = 1), and a PyTorch-eager
+        # unchunked SwiGLU (gate, up, silu, product, down all materialised; memory comparator only)
+        result["peak_activation_same_lib_c_eq_s_gb"] = measure_peak_activation(wl, S) / 1e9
+        result["peak_activation_torch_eager_unchunked_gb"] = measure_eager_unchunked(wl) / 1e9
 
     # end to end through the public API with host buffers (H2D of x, D2H of logits + token)
     if not args.no_e2e:

@@ -87,6 +87,16 @@ class LaunchTimer:
                         self.events[2 * j].elapsed_time(self.events[2 * j + 1])))
         return out
 
+    def timeline(self, origin):
+        """[(kind_name, start_ms, end_ms)] relative to the torch.cuda.Event `origin` (recorded on
+        the same stream before the launches); shows the gaps between launches."""
+        out = []
+        for j in range(min(self._count.value, self.capacity)):
+            out.append((KIND_NAMES.get(self._kinds[j], str(self._kinds[j])),
+                        origin.elapsed_time(self.events[2 * j]), origin.elapsed_time(self.events[2 * j + 1])))
+        return out
+
+
 _lib = None
 
 
