@@ -6,8 +6,10 @@
 //   * lm_head: logits = W_head . rmsnorm(h) and the greedy token
 //       streams W_head (V*d*w bytes) once; per-block packed (value, index) maxima, then a
 //       one-block reduction.  Ties -> lowest index.
-// All are bandwidth-bound: one warp per weight row, 16-byte coalesced vector loads issued
-// in unrolled batches (8 x 16 B in flight per lane), fp32 accumulation, shuffle reductions.
+// All are bandwidth-bound: a warp streams a few weight rows at once (rows_dot: the vector
+// slice each lane needs is read once and reused for every row, so shared-memory / L1 reads do not
+// limit the rate when the SM clock is low under the power cap), 16-byte coalesced vector loads,
+// 8 x 16 B in flight per lane, fp32 accumulation, shuffle reductions.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -21,7 +23,6 @@ namespace gemv {
 
 constexpr int THREADS = 256;
 constexpr int WARPS = THREADS / 32;
-constexpr int UNROLL = 8;
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -57,104 +58,68 @@ __device__ __forceinline__ float dot4_f32(const uint4 &w, const float *x) {
   return s;
 }
 
-// Warp-level dot product of one weight row (n elements, 16-B aligned) with xs (smem fp32).
-template <bool BF16>
-__device__ __forceinline__ float row_dot(const void *wrow, const float *xs, int n, int lane) {
-  constexpr int EPV = BF16 ? 8 : 4;  // elements per 16-B vector
-  const int nvec = n / EPV;
-  const uint4 *w = reinterpret_cast<const uint4 *>(wrow);
-  float acc = 0.f;
-  int v0 = 0;
-  for (; v0 + 32 * UNROLL <= nvec; v0 += 32 * UNROLL) {
-    uint4 buf[UNROLL];
-#pragma unroll
-    for (int u = 0; u < UNROLL; ++u) buf[u] = ld_stream(w + v0 + u * 32 + lane);
-#pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
-      const int e = (v0 + u * 32 + lane) * EPV;
-      acc += BF16 ? dot8_bf16(buf[u], xs + e) : dot4_f32(buf[u], xs + e);
-    }
-  }
-  for (int v = v0 + lane; v < nvec; v += 32) {
-    uint4 b = ld_stream(w + v);
-    const int e = v * EPV;
-    acc += BF16 ? dot8_bf16(b, xs + e) : dot4_f32(b, xs + e);
-  }
-  return warp_sum(acc);
-}
-
-// Two rows (gate and up) against the same smem vector, their loads interleaved so each lane
-// keeps 2 * UNROLL 16-B requests in flight.
-template <bool BF16>
-__device__ __forceinline__ void row_dot2(const void *wrow0, const void *wrow1, const float *xs, int n, int lane,
-                                         float &out0, float &out1) {
+// R consecutive rows of each of NM weight matrices (same row pitch `pitch` bytes) against the
+// same fp32 vector x (shared memory, or global through L1 when XG): each lane reads its slice of x
+// ONCE per step and uses it for all NM * R rows (NM * R x fewer x reads per weight byte than
+// row_dot), with NM * R * UNROLL_R 16-B weight loads in flight.  Rows >= nrows are clamped to
+// the last valid row (their results are discarded).  Per row, the summation order is fixed
+// (ascending 16-B vector index per lane, then the warp_sum butterfly) and does not depend on R,
+// NM or the grid, so a row's result is the same whichever warp computes it (f2's shards).
+template <bool BF16, int NM, int R, bool XG, int UNROLL_R = 2>
+__device__ __forceinline__ void rows_dot(const char *const (&base)[NM], size_t pitch, int nrows,
+                                         const float *__restrict__ x, int n, int lane, float (&out)[NM][R]) {
   constexpr int EPV = BF16 ? 8 : 4;
   const int nvec = n / EPV;
-  const uint4 *w0 = reinterpret_cast<const uint4 *>(wrow0);
-  const uint4 *w1 = reinterpret_cast<const uint4 *>(wrow1);
-  float a0 = 0.f, a1 = 0.f;
-  int v0 = 0;
-  for (; v0 + 32 * UNROLL <= nvec; v0 += 32 * UNROLL) {
-    uint4 b0[UNROLL], b1[UNROLL];
+  int off[R];  // row offsets in 16-B vectors (32-bit: fewer registers than NM * R pointers)
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
-      b0[u] = ld_stream(w0 + v0 + u * 32 + lane);
-      b1[u] = ld_stream(w1 + v0 + u * 32 + lane);
-    }
+  for (int r = 0; r < R; ++r) off[r] = (r < nrows ? r : nrows - 1) * static_cast<int>(pitch / 16);
+  float acc[NM][R];
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
-      const int e = (v0 + u * 32 + lane) * EPV;
-      a0 += BF16 ? dot8_bf16(b0[u], xs + e) : dot4_f32(b0[u], xs + e);
-      a1 += BF16 ? dot8_bf16(b1[u], xs + e) : dot4_f32(b1[u], xs + e);
-    }
-  }
-  for (int v = v0 + lane; v < nvec; v += 32) {
-    const int e = v * EPV;
-    const uint4 c0 = ld_stream(w0 + v), c1 = ld_stream(w1 + v);
-    a0 += BF16 ? dot8_bf16(c0, xs + e) : dot4_f32(c0, xs + e);
-    a1 += BF16 ? dot8_bf16(c1, xs + e) : dot4_f32(c1, xs + e);
-  }
-  out0 = warp_sum(a0);
-  out1 = warp_sum(a1);
-}
-
-// Dot of one weight row with an fp32 vector read through the read-only/L1 path (no smem
-// staging: every block starts streaming weights immediately).
-template <bool BF16>
-__device__ __forceinline__ float row_dot_gvec(const void *wrow, const float *__restrict__ hv, int n, int lane) {
-  constexpr int EPV = BF16 ? 8 : 4;
-  const int nvec = n / EPV;
-  const uint4 *w = reinterpret_cast<const uint4 *>(wrow);
-  float acc = 0.f;
-  int v0 = 0;
-  for (; v0 + 32 * UNROLL <= nvec; v0 += 32 * UNROLL) {
-    uint4 buf[UNROLL];
+  for (int m = 0; m < NM; ++m)
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) buf[u] = ld_stream(w + v0 + u * 32 + lane);
-#pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
-      const int e = (v0 + u * 32 + lane) * EPV;
-      float xv[EPV];
-#pragma unroll
-      for (int q = 0; q < EPV / 4; ++q) {
-        const float4 f = __ldg(reinterpret_cast<const float4 *>(hv + e) + q);
-        xv[4 * q] = f.x; xv[4 * q + 1] = f.y; xv[4 * q + 2] = f.z; xv[4 * q + 3] = f.w;
-      }
-      acc += BF16 ? dot8_bf16(buf[u], xv) : dot4_f32(buf[u], xv);
-    }
-  }
-  for (int v = v0 + lane; v < nvec; v += 32) {
-    const uint4 b = ld_stream(w + v);
-    const int e = v * EPV;
-    float xv[EPV];
+    for (int r = 0; r < R; ++r) acc[m][r] = 0.f;
+  auto load_x = [&](int e, float (&xv)[EPV]) {
 #pragma unroll
     for (int q = 0; q < EPV / 4; ++q) {
-      const float4 f = __ldg(reinterpret_cast<const float4 *>(hv + e) + q);
+      const float4 f = XG ? __ldg(reinterpret_cast<const float4 *>(x + e) + q) : reinterpret_cast<const float4 *>(x + e)[q];
       xv[4 * q] = f.x; xv[4 * q + 1] = f.y; xv[4 * q + 2] = f.z; xv[4 * q + 3] = f.w;
     }
-    acc += BF16 ? dot8_bf16(b, xv) : dot4_f32(b, xv);
+  };
+  int v0 = 0;
+  for (; v0 + 32 * UNROLL_R <= nvec; v0 += 32 * UNROLL_R) {
+    uint4 buf[UNROLL_R][NM][R];
+#pragma unroll
+    for (int u = 0; u < UNROLL_R; ++u)
+#pragma unroll
+      for (int m = 0; m < NM; ++m)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          buf[u][m][r] = ld_stream(reinterpret_cast<const uint4 *>(base[m]) + off[r] + v0 + u * 32 + lane);
+#pragma unroll
+    for (int u = 0; u < UNROLL_R; ++u) {
+      float xv[EPV];
+      load_x((v0 + u * 32 + lane) * EPV, xv);
+#pragma unroll
+      for (int m = 0; m < NM; ++m)
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[m][r] += BF16 ? dot8_bf16(buf[u][m][r], xv) : dot4_f32(buf[u][m][r], xv);
+    }
   }
-  return warp_sum(acc);
+  for (int v = v0 + lane; v < nvec; v += 32) {
+    float xv[EPV];
+    load_x(v * EPV, xv);
+#pragma unroll
+    for (int m = 0; m < NM; ++m)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint4 b = ld_stream(reinterpret_cast<const uint4 *>(base[m]) + off[r] + v);
+        acc[m][r] += BF16 ? dot8_bf16(b, xv) : dot4_f32(b, xv);
+      }
+  }
+#pragma unroll
+  for (int m = 0; m < NM; ++m)
+#pragma unroll
+    for (int r = 0; r < R; ++r) out[m][r] = warp_sum(acc[m][r]);
 }
 
 template <bool BF16>
@@ -220,43 +185,55 @@ __device__ __forceinline__ void prefetch_my_rows(const void *base, size_t pitch,
   }
 }
 
-// h[j] = Swish(sum_k x_k Wg[j,k]) * (sum_k x_k Wu[j,k]), fp32.  Grid-stride over rows j.
-template <bool BF16>
-__global__ void __launch_bounds__(THREADS) gate_up_gemv(const void *__restrict__ x, const void *__restrict__ wg,
-                                                        const void *__restrict__ wu, float *__restrict__ h, int d,
-                                                        int I) {
-  pdl_launch_dependents();  // the down GEMV may launch now and prefetch W_down
+// h[j] = Swish(sum_k x_k Wg[j,k]) * (sum_k x_k Wu[j,k]), fp32.  Warp-stride over groups of R
+// rows j (gate and up rows of each j streamed together).
+template <bool BF16, int R>
+__global__ void __launch_bounds__(THREADS, 4) gate_up_gemv(const void *__restrict__ x, const void *__restrict__ wg,
+                                                           const void *__restrict__ wu, float *__restrict__ h, int d,
+                                                           int I) {
+  pdl_launch_dependents();  // the down GEMV may launch now
   extern __shared__ float xs[];
   stage_vec<BF16>(x, xs, d);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int w = blockIdx.x * WARPS + (threadIdx.x >> 5);
   const size_t pitch = static_cast<size_t>(d) * (BF16 ? 2 : 4);
-  for (int j = w; j < I; j += gridDim.x * WARPS) {
-    float g, u;
-    row_dot2<BF16>(static_cast<const char *>(wg) + j * pitch, static_cast<const char *>(wu) + j * pitch, xs, d,
-                   lane, g, u);
-    if (lane == 0) h[j] = g / (1.0f + __expf(-g)) * u;
+  for (int j0 = w * R; j0 < I; j0 += gridDim.x * WARPS * R) {
+    float gu[2][R];
+    const char *const base[2] = {static_cast<const char *>(wg) + j0 * pitch, static_cast<const char *>(wu) + j0 * pitch};
+    rows_dot<BF16, 2, R, false>(base, pitch, I - j0, xs, d, lane, gu);
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (j0 + r < I) h[j0 + r] = gu[0][r] / (1.0f + __expf(-gu[0][r])) * gu[1][r];
+    }
   }
 }
 
 // out[c] = residual[c] + sum_j h_j Wd[c,j].  h (fp32) read through L1 (no staging barrier).
-template <bool BF16>
-__global__ void __launch_bounds__(THREADS) down_gemv(const float *__restrict__ h, const void *__restrict__ wd,
-                                                     const void *__restrict__ residual, void *__restrict__ out, int d,
-                                                     int I, int prefetch_rows) {
+template <bool BF16, int R>
+__global__ void __launch_bounds__(THREADS, 4) down_gemv(const float *__restrict__ h, const void *__restrict__ wd,
+                                                        const void *__restrict__ residual, void *__restrict__ out,
+                                                        int d, int I, int prefetch_rows) {
   const int lane = threadIdx.x & 31;
   const int w = blockIdx.x * WARPS + (threadIdx.x >> 5);
   const size_t pitch = static_cast<size_t>(I) * (BF16 ? 2 : 4);
-  // W_down does not depend on h: pull this warp's rows towards L2 while gate/up still runs
+  // W_down does not depend on h: optionally pull this warp's rows towards L2 while gate/up runs
   if ((pitch & 15) == 0 && prefetch_rows > 0) prefetch_my_rows(wd, pitch, d, prefetch_rows);
   pdl_launch_dependents();  // the LM head may launch early too
   pdl_wait();               // h (written by gate_up_gemv) is complete and visible from here on
-  for (int c = w; c < d; c += gridDim.x * WARPS) {
-    const float o = row_dot_gvec<BF16>(static_cast<const char *>(wd) + c * pitch, h, I, lane);
+  for (int c0 = w * R; c0 < d; c0 += gridDim.x * WARPS * R) {
+    float o[1][R];
+    const char *const base[1] = {static_cast<const char *>(wd) + c0 * pitch};
+    rows_dot<BF16, 1, R, true>(base, pitch, d - c0, h, I, lane, o);
     if (lane == 0) {
-      const float r = residual ? load_elem<BF16>(residual, c) : 0.f;
-      store_elem<BF16>(out, c, r + o);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (c0 + r < d) {
+          const float rv = residual ? load_elem<BF16>(residual, c0 + r) : 0.f;
+          store_elem<BF16>(out, c0 + r, rv + o[0][r]);
+        }
+      }
     }
   }
 }
@@ -279,8 +256,8 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
   return v;
 }
 
-template <bool BF16>
-__global__ void __launch_bounds__(THREADS) lm_head_gemv(const void *__restrict__ hin, const void *__restrict__ gain,
+template <bool BF16, int R, int U>
+__global__ void __launch_bounds__(THREADS, 4) lm_head_gemv(const void *__restrict__ hin, const void *__restrict__ gain,
                                                         float eps, const void *__restrict__ w,
                                                         float *__restrict__ logits,
                                                         unsigned long long *__restrict__ partials, int d, int V,
@@ -306,12 +283,20 @@ __global__ void __launch_bounds__(THREADS) lm_head_gemv(const void *__restrict__
   const int wglob = blockIdx.x * WARPS + wid;
   const size_t pitch = static_cast<size_t>(d) * (BF16 ? 2 : 4);
   unsigned long long best = 0ull;
-  for (int v = wglob; v < V; v += gridDim.x * WARPS) {
-    const float s = row_dot<BF16>(static_cast<const char *>(w) + v * pitch, hs, d, lane);
+  // warp-stride over groups of R consecutive rows
+  for (int v0 = wglob * R; v0 < V; v0 += gridDim.x * WARPS * R) {
+    float s[1][R];
+    const char *const base[1] = {static_cast<const char *>(w) + v0 * pitch};
+    rows_dot<BF16, 1, R, false, U>(base, pitch, V - v0, hs, d, lane, s);
     if (lane == 0) {
-      if (logits) logits[v] = s;
-      const unsigned long long key = pack_key(s, v + vocab_offset);  // global vocab index
-      best = key > best ? key : best;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (v0 + r < V) {
+          if (logits) logits[v0 + r] = s[0][r];
+          const unsigned long long key = pack_key(s[0][r], v0 + r + vocab_offset);  // global vocab index
+          best = key > best ? key : best;
+        }
+      }
     }
   }
   if (lane == 0) best_s[wid] = best;
@@ -398,20 +383,23 @@ cudaError_t launch_last_token_mlp(const void *x, const void *residual, const voi
     const int warps = (rows + r - 1) / r;
     return (warps + WARPS - 1) / WARPS;
   };
-  const int blocks1 = balanced_blocks(I, 6);
-  const int blocks2 = balanced_blocks(d, 6);
+  constexpr int RG = 2, RD = 2;  // rows per warp step: gate/up (x 2 matrices), down
+  const int blocks1 = balanced_blocks((I + RG - 1) / RG, 4);
+  const int blocks2 = balanced_blocks((d + RD - 1) / RD, 4);
   const bool pdl = env_or("MOM_GEMV_PDL", 1) != 0;     // PDL launch of the down GEMV
   const int pf = env_or("MOM_GEMV_PREFETCH", 0);        // W_down rows per warp prefetched to L2 first
   cudaError_t e;
   if (is_bf16) {
-    if ((e = set_smem(gate_up_gemv<true>, smem1)) != cudaSuccess) return e;
-    gate_up_gemv<true><<<blocks1, THREADS, smem1, stream>>>(x, wg, wu, h_ws, d, I);
-    if ((e = launch_maybe_pdl(down_gemv<true>, blocks2, 0, stream, pdl, h_ws, wd, residual, out, d, I, pf)) != cudaSuccess)
+    if ((e = set_smem(gate_up_gemv<true, RG>, smem1)) != cudaSuccess) return e;
+    gate_up_gemv<true, RG><<<blocks1, THREADS, smem1, stream>>>(x, wg, wu, h_ws, d, I);
+    if ((e = launch_maybe_pdl(down_gemv<true, RD>, blocks2, 0, stream, pdl, h_ws, wd, residual, out, d, I, pf)) !=
+        cudaSuccess)
       return e;
   } else {
-    if ((e = set_smem(gate_up_gemv<false>, smem1)) != cudaSuccess) return e;
-    gate_up_gemv<false><<<blocks1, THREADS, smem1, stream>>>(x, wg, wu, h_ws, d, I);
-    if ((e = launch_maybe_pdl(down_gemv<false>, blocks2, 0, stream, pdl, h_ws, wd, residual, out, d, I, pf)) != cudaSuccess)
+    if ((e = set_smem(gate_up_gemv<false, RG>, smem1)) != cudaSuccess) return e;
+    gate_up_gemv<false, RG><<<blocks1, THREADS, smem1, stream>>>(x, wg, wu, h_ws, d, I);
+    if ((e = launch_maybe_pdl(down_gemv<false, RD>, blocks2, 0, stream, pdl, h_ws, wd, residual, out, d, I, pf)) !=
+        cudaSuccess)
       return e;
   }
   return cudaGetLastError();
@@ -425,19 +413,23 @@ cudaError_t launch_lm_head(const void *h, const void *gain, float eps, const voi
                            cudaStream_t stream) {
   using namespace gemv;
   const size_t smem = static_cast<size_t>(d) * sizeof(float);
-  int blocks = static_cast<int>(lm_head_partials(num_sms));
-  const int need = (V + WARPS - 1) / WARPS;
-  if (blocks > need) blocks = need;
+  // 4 rows per warp step (x reused from registers across them) x 2 16-B loads in flight per row
+  // (measured: 2 rows x 4 loads is equivalent, tools/head_variants.sh)
+  constexpr int R = 4, U = 2;
+  // balanced single wave (4 blocks per SM resident): every warp gets r or r - 1 row groups
+  const int groups = (V + R - 1) / R;
+  const int resident = static_cast<int>(lm_head_partials(num_sms)) * WARPS;
+  const int r = (groups + resident - 1) / resident;
+  const int blocks = ((groups + r - 1) / r + WARPS - 1) / WARPS;
   cudaError_t e;
   if (is_bf16) {
-    if ((e = set_smem(lm_head_gemv<true>, smem)) != cudaSuccess) return e;
-    e = launch_pdl(lm_head_gemv<true>, blocks, smem, stream, h, gain, eps, w, logits, partials, d, V, vocab_offset);
-    if (e != cudaSuccess) return e;
+    if ((e = set_smem(lm_head_gemv<true, R, U>, smem)) != cudaSuccess) return e;
+    e = launch_pdl(lm_head_gemv<true, R, U>, blocks, smem, stream, h, gain, eps, w, logits, partials, d, V, vocab_offset);
   } else {
-    if ((e = set_smem(lm_head_gemv<false>, smem)) != cudaSuccess) return e;
-    e = launch_pdl(lm_head_gemv<false>, blocks, smem, stream, h, gain, eps, w, logits, partials, d, V, vocab_offset);
-    if (e != cudaSuccess) return e;
+    if ((e = set_smem(lm_head_gemv<false, R, U>, smem)) != cudaSuccess) return e;
+    e = launch_pdl(lm_head_gemv<false, R, U>, blocks, smem, stream, h, gain, eps, w, logits, partials, d, V, vocab_offset);
   }
+  if (e != cudaSuccess) return e;
   argmax_reduce<<<1, 1024, 0, stream>>>(partials, blocks, argmax, key_out);
   return cudaGetLastError();
 }
