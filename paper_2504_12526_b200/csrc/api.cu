@@ -269,6 +269,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
   // tail but runs phase-A and phase-B tiles concurrently, which costs more DRAM traffic, and on
   // the power-capped B200 that energy costs more clock than the tail (energy sweep, round 1).
   const bool fused = env_int("MOM_FUSED", 0) != 0;
+  const bool mlp_pdl = env_int("MOM_MLP_PDL", 1) != 0;
   CUtensorMap tm_wg, tm_wu, tm_wd;
   mom_status_t st;
   if (dt == MOM_BF16) {
@@ -370,6 +371,10 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
       continue;
     }
     a.group_m = group_a;
+    // PDL: phase A of mini-sequence i > 0 may start on the SMs the previous phase B frees and
+    // stream X_i / weights while that phase B finishes (its epilogue waits before storing H_i);
+    // phase B may start its prologue under phase A's tail.  Not after a host->device wait.
+    a.pdl = mlp_pdl && i > 0 && !x_host;
     {
       ScopedTiming tm(stream, 0);
       e = mom::launch_mlp_tc(a, 0, stream);  // H_i = Swish(A_i Wg^T) (.) A_i Wu^T
@@ -378,6 +383,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     a.group_m = group_b;
     a.fwd_src = nullptr;  // forwarding rides on the phase-A launch only
     a.n_fwd = 0;
+    a.pdl = mlp_pdl;
     {
       ScopedTiming tm(stream, 1);
       e = mom::launch_mlp_tc(a, 1, stream);  // O_i = R_i + H_i Wd^T, written at rows r0..

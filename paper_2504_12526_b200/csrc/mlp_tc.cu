@@ -108,6 +108,9 @@ struct Tile {
   bool a;  // phase A tile
 };
 
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <int MODE>
 __device__ __forceinline__ Tile decode_tile(uint32_t t, const Params &p) {
   Tile tl;
@@ -406,6 +409,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // PDL (split mode): let the next launch in the stream start as soon as SMs free up; its CTAs
+  // run their prologue and whatever does not depend on this launch, then griddepcontrol.wait.
+  // Both are no-ops when the launches carry no programmatic-serialization attribute.
+  if (MODE != MODE_FUSED) pdl_launch_dependents();
 
   if (warp == 0) {
     // ======================= TMA producer =======================
@@ -416,6 +423,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t pol_norm = ptx::policy_evict_normal();
       const uint64_t pol_first = ptx::policy_evict_first();
       const uint32_t full_leader0 = (CG == 2) ? ptx::mapa(ptx::smem_u32(&full[0]), 0) : ptx::smem_u32(&full[0]);
+      // phase B reads H_i, written by the preceding phase-A launch: wait for it (and, through its
+      // own epilogue wait, for everything before it).  Phase A reads only X_i and the weights.
+      if (MODE == MODE_B) pdl_wait();
       uint32_t stage = 0, phase = 0;
       for (uint32_t t = cluster_id; t < num_tiles; t += num_clusters) {
         const Tile tl = decode_tile<MODE>(t, p);
@@ -511,6 +521,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t row_in_tile = q * 32 + lane;
     uint32_t acc = 0, acc_phase = 0;
     const uint32_t tempty_leader = (CG == 2) ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0;
+    // phase A writes H_i, which the preceding phase-B launch (previous mini-sequence) reads, and
+    // reads row_scale; phase B writes O_i: no epilogue store before the previous launch completed
+    pdl_wait();
     for (uint32_t t = cluster_id; t < num_tiles; t += num_clusters) {
       const Tile tl = decode_tile<MODE>(t, p);
       ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -549,6 +562,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // Its output rows are final (the previous launch completed); copy this CTA's share of them
     // to every peer while the tensor cores work on this mini-sequence.  64 threads per CTA,
     // 16-B units, 4 independent loads in flight per thread.
+    pdl_wait();  // the rows are final once the previous launch (its phase B) completed
     const uint32_t tid = threadIdx.x - 64;  // 0..63
     const size_t units = static_cast<size_t>(p.fwd_rows) * (p.d / 8);
     const size_t per_cta = (units + gridDim.x - 1) / gridDim.x;
@@ -576,7 +590,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 template <int CG, int MODE>
-static cudaError_t launch(const Maps &maps, const Params &p, int num_sms, cudaStream_t stream) {
+static cudaError_t launch(const Maps &maps, const Params &p, int num_sms, bool pdl, cudaStream_t stream) {
   using C = Cfg<CG>;
   auto kfn = mlp_tc_kernel<CG, MODE>;
   static thread_local int configured_device = -1;  // attribute is per device
@@ -597,13 +611,15 @@ static cudaError_t launch(const Maps &maps, const Params &p, int num_sms, cudaSt
   cfg.blockDim = dim3(NUM_THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kfn, maps, p);
 }
 
@@ -640,8 +656,9 @@ static cudaError_t launch_mode(const TcMlpArgs &a, cudaStream_t stream) {
   for (uint32_t k = 0; k < p.n_fwd && k < kMaxPeers; ++k) p.fwd_dst[k] = a.fwd_dst[k];
   p.n_peers = a.n_peers;
   for (uint32_t k = 0; k < a.n_peers && k < kMaxPeers; ++k) p.peer_out[k] = a.peer_out[k];
-  if (a.cta_group == 2) return launch<2, MODE>(maps, p, a.num_sms, stream);
-  return launch<1, MODE>(maps, p, a.num_sms, stream);
+  const bool pdl = a.pdl && MODE != MODE_FUSED;
+  if (a.cta_group == 2) return launch<2, MODE>(maps, p, a.num_sms, pdl, stream);
+  return launch<1, MODE>(maps, p, a.num_sms, pdl, stream);
 }
 
 }  // namespace tc

@@ -25,7 +25,8 @@ kv_back = torch.empty_like(kv)
 host_a = torch.empty(kv.shape, dtype=bf, pin_memory=True)
 host_b = torch.empty(kv.shape, dtype=bf, pin_memory=True)
 compute, s_d2h, s_h2d = (torch.cuda.Stream(dev) for _ in range(3))
-modes = ["none", "d2h", "h2d", "both"]
+modes = ["none", "d2h", "h2d", "both", "both_spread"]
+M = (S + C - 1) // C
 res = {m: [] for m in modes}
 for r in range(4):
     for m in modes:
@@ -38,7 +39,20 @@ for r in range(4):
             if m in ("h2d", "both"):
                 s_h2d.wait_stream(compute)
                 _mom.kv_reload(host_b, kv_back, s_h2d)
-            _mom.mlp_minseq_fwd(x, x, wg, wu, wd, out, C, ws, compute)
+            if m == "both_spread":
+                # one mini-sequence per call; chunk i of each copy waits for mini-sequence i-1
+                rows = kv.shape[0]
+                for i in range(M):
+                    if i > 0:
+                        s_d2h.wait_stream(compute)
+                        s_h2d.wait_stream(compute)
+                    r0, r1 = i * rows // M, (i + 1) * rows // M
+                    _mom.kv_offload(kv[r0:r1], host_a[r0:r1], compute, s_d2h)
+                    _mom.kv_reload(host_b[r0:r1], kv_back[r0:r1], s_h2d)
+                    _mom.mlp_minseq_fwd(x[i * C:(i + 1) * C], x[i * C:(i + 1) * C], wg, wu, wd,
+                                        out[i * C:(i + 1) * C], C, ws, compute)
+            else:
+                _mom.mlp_minseq_fwd(x, x, wg, wu, wd, out, C, ws, compute)
         torch.cuda.synchronize()
         res[m].append([t for _, t in timer.results()])
 for m in modes:
