@@ -114,7 +114,12 @@ mom_status_t mom_mlp_minseq_fwd(const void *x, const void *residual, const void 
  * mini-sequence i the rows of A_i are copied x_host_pinned -> x (device [S, hidden]) on
  * copy_stream, and `stream` waits for exactly those rows before computing O_i, so the PCIe
  * transfer of A_{i+1} overlaps the tensor-core work on A_i (the partition of P:109 applied to
- * the host->device input).  copy_stream first waits for work already queued on `stream`.
+ * the host->device input).
+ *   x_free     NULL: copy_stream first waits for all work already queued on `stream` (safe
+ *              whatever else reads x).  Else a caller-recorded cudaEvent_t after which nothing
+ *              reads or writes x: copy_stream waits on it instead, so the input of the next
+ *              request can stream in while `stream` still runs earlier requests (prefetch; the
+ *              caller double-buffers x).  A never-recorded event does not delay the copies.
  * residual may equal x (the usual x + MLP(x)).  x_host_pinned must be page-locked (checked);
  * copy_stream must differ from stream.  Other arguments and errors as mom_mlp_minseq_fwd. */
 mom_status_t mom_mlp_minseq_fwd_from_host(const void *x_host_pinned, void *x, const void *residual,
@@ -122,7 +127,7 @@ mom_status_t mom_mlp_minseq_fwd_from_host(const void *x_host_pinned, void *x, co
                                           void *out, int64_t S, int64_t hidden, int64_t intermediate,
                                           int64_t minseq_len, mom_dtype_t dt, void *workspace,
                                           size_t workspace_bytes, mom_stream_t stream,
-                                          mom_stream_t copy_stream);
+                                          mom_stream_t copy_stream, mom_event_t x_free);
 
 /* ------------------------------------------------------------------------------------
  * f3. The per-layer RMSNorm folded into the mini-sequence MLP: the Llama

@@ -26,7 +26,7 @@ SIGNATURES = {
     "mom_mlp_minseq_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64, _i32]),
     "mom_mlp_minseq_fwd": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i32, _p, _sz, _p]),
     "mom_mlp_minseq_fwd_from_host": (_i32, [_p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i32, _p, _sz, _p,
-                                            _p]),
+                                            _p, _p]),
     "mom_fold_norm_gain": (_i32, [_p, _p, _p, _i64, _i64, _i32, _p]),
     "mom_mlp_minseq_rmsnorm_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64, _i32]),
     "mom_mlp_minseq_rmsnorm_fwd": (_i32, [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _f32, _i32, _p, _sz, _p]),
@@ -192,9 +192,10 @@ def mlp_minseq_fwd(x, residual, w_gate, w_up, w_down, out, minseq_len: int, work
 
 
 def mlp_minseq_fwd_from_host(x_host, x, residual, w_gate, w_up, w_down, out, minseq_len: int, workspace=None,
-                             stream=None, copy_stream=None):
+                             stream=None, copy_stream=None, x_free=None):
     """End-to-end entry: x_host (pinned) is streamed into x one mini-sequence at a time on
-    copy_stream while the MLP of the previous mini-sequence runs on stream."""
+    copy_stream while the MLP of the previous mini-sequence runs on stream.  x_free: optional
+    torch.cuda.Event after which x is free (the copies wait on it instead of on `stream`)."""
     S, hidden = x.shape
     I = w_gate.shape[0]
     dt = _dt(x)
@@ -206,7 +207,8 @@ def mlp_minseq_fwd_from_host(x_host, x, residual, w_gate, w_up, w_down, out, min
     ws_bytes = workspace.numel() * workspace.element_size()
     _check(lib().mom_mlp_minseq_fwd_from_host(_ptr(x_host), _ptr(x), _ptr(residual), _ptr(w_gate), _ptr(w_up),
                                               _ptr(w_down), _ptr(out), S, hidden, I, minseq_len, dt, _ptr(workspace),
-                                              ws_bytes, _stream(stream), _stream(copy_stream)))
+                                              ws_bytes, _stream(stream), _stream(copy_stream),
+                                              _event_handle(x_free)))
     return out
 
 

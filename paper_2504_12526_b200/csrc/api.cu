@@ -478,7 +478,7 @@ mom_status_t mom_mlp_minseq_fwd_from_host(const void *x_host_pinned, void *x, co
                                           const void *w_gate, const void *w_up, const void *w_down, void *out,
                                           int64_t S, int64_t hidden, int64_t intermediate, int64_t C,
                                           mom_dtype_t dt, void *workspace, size_t workspace_bytes,
-                                          mom_stream_t stream, mom_stream_t copy_stream) {
+                                          mom_stream_t stream, mom_stream_t copy_stream, mom_event_t x_free) {
   g_err[0] = 0;
   if (!x_host_pinned) return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd_from_host: null host pointer");
   mom_status_t st = validate_minseq("mom_mlp_minseq_fwd_from_host", x, residual, w_gate, w_up, w_down, out, S,
@@ -487,6 +487,13 @@ mom_status_t mom_mlp_minseq_fwd_from_host(const void *x_host_pinned, void *x, co
   if ((st = check_pinned(x_host_pinned, "mom_mlp_minseq_fwd_from_host")) != MOM_OK) return st;
   if (copy_stream == stream) return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd_from_host: copy_stream must differ from stream");
   cudaStream_t s = static_cast<cudaStream_t>(stream), cp = static_cast<cudaStream_t>(copy_stream);
+  if (x_free) {
+    // the caller names the point after which x is free (double-buffered inputs: prefetch)
+    cudaError_t e = cudaStreamWaitEvent(cp, static_cast<cudaEvent_t>(x_free), 0);
+    if (e != cudaSuccess) return cuda_fail(e, "x_free ordering");
+    return run_minseq(x, residual, w_gate, w_up, w_down, out, S, hidden, intermediate, C, dt, workspace, s,
+                      x_host_pinned, cp);
+  }
   // the copy stream must not start writing x before earlier work on `stream` is done with it
   cudaEvent_t ready;
   cudaError_t e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);

@@ -115,7 +115,7 @@ def test_new_entry_points_reject_bad_arguments(lib):
     assert lib.mom_mlp_minseq_fwd_gather(16, None, 32, 48, 64, 80, peers, 8, 4, 8, 16, 2, 0, 96, 1 << 20, None) == E
     # from_host: null host pointer
     assert lib.mom_mlp_minseq_fwd_from_host(None, 16, None, 32, 48, 64, 80, 4, 8, 16, 2, 0, 96, 1 << 20, None,
-                                            None) == E
+                                            None, None) == E
     # folded norm: fp32 unsupported, bad eps, misaligned
     assert lib.mom_fold_norm_gain(16, 32, 48, 4, 8, _mom.MOM_F32, None) == U
     assert lib.mom_fold_norm_gain(16, 32, 48, 4, 6, _mom.MOM_BF16, None) == E

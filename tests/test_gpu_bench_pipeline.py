@@ -46,6 +46,8 @@ def test_pipelined_steps_equal_one_request(cuda_device, e2e, serial):
     compute, copy, reload = (torch.cuda.Stream(cuda_device) for _ in range(3))
     h2d = torch.cuda.Stream(cuda_device)
     x_host = wl.x.cpu().pin_memory() if e2e else None
+    if e2e:
+        wl.init_e2e(compute)  # double-buffered device input (the second buffer starts empty)
     wl.out.zero_()
     wl.kv_back.zero_()
     with torch.cuda.stream(compute):

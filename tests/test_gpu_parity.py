@@ -259,6 +259,35 @@ def test_from_host_streamed_equals_device_input(cuda_device):
         _mom.mlp_minseq_fwd_from_host(x.clone(), x_dev, x_dev, g[2], g[3], g[4], out, C, copy_stream=cp)
 
 
+def test_from_host_prefetch_double_buffered(cuda_device):
+    """x_free (prefetch): consecutive requests alternate two device input buffers and each
+    request's H2D waits only for the request that last used its buffer, so it streams in while the
+    previous request computes.  Every request's output equals the device-input call bitwise."""
+    S, d, I, C = 1000, 256, 688, 300
+    (x, res, wg, wu, wd), g = _mlp_inputs(S, d, I, torch.bfloat16, cuda_device, residual=False)
+    xs = [x, (x * -0.5).to(torch.bfloat16), (x * 2).to(torch.bfloat16)]
+    refs = []
+    for xi in xs:
+        xd = xi.to(cuda_device)
+        refs.append(_run_fwd(xd, xd, *g[2:], C=C))
+    hosts = [xi.pin_memory() for xi in xs]
+    bufs = [torch.zeros_like(g[0]) for _ in range(2)]
+    outs = [torch.empty_like(g[0]) for _ in range(6)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    compute, cp = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(compute):
+        for e in free:
+            e.record(compute)
+        for r in range(6):
+            slot = r % 2
+            _mom.mlp_minseq_fwd_from_host(hosts[r % 3], bufs[slot], bufs[slot], g[2], g[3], g[4], outs[r], C,
+                                          stream=compute, copy_stream=cp, x_free=free[slot])
+            free[slot].record(compute)
+    torch.cuda.synchronize()
+    for r in range(6):
+        assert torch.equal(outs[r], refs[r % 3]), r
+
+
 # ------------------------------------------------------------------ f3: RMSNorm folded into phase A
 @pytest.mark.parametrize("S,d,I,C", [(1000, 512, 1024, 300), (4096, 4096, 14336, 2048)])
 def test_rmsnorm_folded_mlp(cuda_device, S, d, I, C):
