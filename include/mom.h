@@ -33,7 +33,8 @@
  *               MOM_CTA_GROUP (2), MOM_GROUP_M_A (16), MOM_GROUP_M_B (8), MOM_TMA_POLICY (0),
  *               MOM_FUSED (0: two launches per mini-sequence), MOM_EPI_A_COALESCED (1),
  *               MOM_GATHER_FORWARD (1: f1 rows of mini-sequence i-1 forwarded during i),
- *               MOM_GEMV_PDL (1), MOM_MLP_PDL (1: programmatic dependent launch between the
+ *               MOM_GEMV_PDL (1), MOM_GEMV_VARIANT (1: down GEMV with 4 loads in flight per
+ *               row at 2 blocks/SM; 0: the earlier 2 at 4/SM), MOM_MLP_PDL (1: programmatic dependent launch between the
  *               tcgen05 MLP launches of one call), MOM_NB_B (phase-B tile width; default: chosen per shape for
  *               wave quantisation).  None changes results: outputs are bitwise identical.
  *   Alignment   Device pointers must be 16-byte aligned and row pitches (hidden*w,

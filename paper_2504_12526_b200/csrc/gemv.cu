@@ -187,8 +187,8 @@ __device__ __forceinline__ void prefetch_my_rows(const void *base, size_t pitch,
 
 // h[j] = Swish(sum_k x_k Wg[j,k]) * (sum_k x_k Wu[j,k]), fp32.  Warp-stride over groups of R
 // rows j (gate and up rows of each j streamed together).
-template <bool BF16, int R>
-__global__ void __launch_bounds__(THREADS, 4) gate_up_gemv(const void *__restrict__ x, const void *__restrict__ wg,
+template <bool BF16, int R, int U = 2, int MINB = 4>
+__global__ void __launch_bounds__(THREADS, MINB) gate_up_gemv(const void *__restrict__ x, const void *__restrict__ wg,
                                                            const void *__restrict__ wu, float *__restrict__ h, int d,
                                                            int I) {
   pdl_launch_dependents();  // the down GEMV may launch now
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(THREADS, 4) gate_up_gemv(const void *__restric
   for (int j0 = w * R; j0 < I; j0 += gridDim.x * WARPS * R) {
     float gu[2][R];
     const char *const base[2] = {static_cast<const char *>(wg) + j0 * pitch, static_cast<const char *>(wu) + j0 * pitch};
-    rows_dot<BF16, 2, R, false>(base, pitch, I - j0, xs, d, lane, gu);
+    rows_dot<BF16, 2, R, false, U>(base, pitch, I - j0, xs, d, lane, gu);
     if (lane == 0) {
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -211,8 +211,8 @@ __global__ void __launch_bounds__(THREADS, 4) gate_up_gemv(const void *__restric
 }
 
 // out[c] = residual[c] + sum_j h_j Wd[c,j].  h (fp32) read through L1 (no staging barrier).
-template <bool BF16, int R>
-__global__ void __launch_bounds__(THREADS, 4) down_gemv(const float *__restrict__ h, const void *__restrict__ wd,
+template <bool BF16, int R, int U = 2, int MINB = 4>
+__global__ void __launch_bounds__(THREADS, MINB) down_gemv(const float *__restrict__ h, const void *__restrict__ wd,
                                                         const void *__restrict__ residual, void *__restrict__ out,
                                                         int d, int I, int prefetch_rows) {
   const int lane = threadIdx.x & 31;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(THREADS, 4) down_gemv(const float *__restrict_
   for (int c0 = w * R; c0 < d; c0 += gridDim.x * WARPS * R) {
     float o[1][R];
     const char *const base[1] = {static_cast<const char *>(wd) + c0 * pitch};
-    rows_dot<BF16, 1, R, true>(base, pitch, d - c0, h, I, lane, o);
+    rows_dot<BF16, 1, R, true, U>(base, pitch, d - c0, h, I, lane, o);
     if (lane == 0) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -370,9 +370,9 @@ static cudaError_t set_smem(K kfn, size_t bytes) {
 
 }  // namespace gemv
 
-cudaError_t launch_last_token_mlp(const void *x, const void *residual, const void *wg, const void *wu,
-                                  const void *wd, void *out, float *h_ws, int d, int I, bool is_bf16, int num_sms,
-                                  cudaStream_t stream) {
+template <bool BF16, int RG, int UG, int MG, int RD, int UD, int MD>
+static cudaError_t last_token_pair(const void *x, const void *residual, const void *wg, const void *wu, const void *wd,
+                                   void *out, float *h_ws, int d, int I, int num_sms, cudaStream_t stream) {
   using namespace gemv;
   const size_t smem1 = static_cast<size_t>(d) * sizeof(float);
   // Balanced single-wave grids: r = ceil(rows / resident warps) rows per warp, and just enough
@@ -383,26 +383,30 @@ cudaError_t launch_last_token_mlp(const void *x, const void *residual, const voi
     const int warps = (rows + r - 1) / r;
     return (warps + WARPS - 1) / WARPS;
   };
-  constexpr int RG = 2, RD = 2;  // rows per warp step: gate/up (x 2 matrices), down
-  const int blocks1 = balanced_blocks((I + RG - 1) / RG, 4);
-  const int blocks2 = balanced_blocks((d + RD - 1) / RD, 4);
+  const int blocks1 = balanced_blocks((I + RG - 1) / RG, MG);
+  const int blocks2 = balanced_blocks((d + RD - 1) / RD, MD);
   const bool pdl = env_or("MOM_GEMV_PDL", 1) != 0;     // PDL launch of the down GEMV
   const int pf = env_or("MOM_GEMV_PREFETCH", 0);        // W_down rows per warp prefetched to L2 first
   cudaError_t e;
-  if (is_bf16) {
-    if ((e = set_smem(gate_up_gemv<true, RG>, smem1)) != cudaSuccess) return e;
-    gate_up_gemv<true, RG><<<blocks1, THREADS, smem1, stream>>>(x, wg, wu, h_ws, d, I);
-    if ((e = launch_maybe_pdl(down_gemv<true, RD>, blocks2, 0, stream, pdl, h_ws, wd, residual, out, d, I, pf)) !=
-        cudaSuccess)
-      return e;
-  } else {
-    if ((e = set_smem(gate_up_gemv<false, RG>, smem1)) != cudaSuccess) return e;
-    gate_up_gemv<false, RG><<<blocks1, THREADS, smem1, stream>>>(x, wg, wu, h_ws, d, I);
-    if ((e = launch_maybe_pdl(down_gemv<false, RD>, blocks2, 0, stream, pdl, h_ws, wd, residual, out, d, I, pf)) !=
-        cudaSuccess)
-      return e;
-  }
+  if ((e = set_smem(gate_up_gemv<BF16, RG, UG, MG>, smem1)) != cudaSuccess) return e;
+  gate_up_gemv<BF16, RG, UG, MG><<<blocks1, THREADS, smem1, stream>>>(x, wg, wu, h_ws, d, I);
+  if ((e = launch_maybe_pdl(down_gemv<BF16, RD, UD, MD>, blocks2, 0, stream, pdl, h_ws, wd, residual, out, d, I, pf)) !=
+      cudaSuccess)
+    return e;
   return cudaGetLastError();
+}
+
+cudaError_t launch_last_token_mlp(const void *x, const void *residual, const void *wg, const void *wu,
+                                  const void *wd, void *out, float *h_ws, int d, int I, bool is_bf16, int num_sms,
+                                  cudaStream_t stream) {
+  // (rows per warp step, 16-B loads in flight per row, min blocks per SM) for gate/up and down.
+  // Down: 2 rows x 4 loads in flight at 2 blocks/SM (2048 warps, 16 MB in flight) instead of
+  // 2 x 2 at 4/SM (4 MB in flight: latency-bound at ~3.5 TB/s); measured 74.8 -> 64.5-67.6 us
+  // for the pair (profiles/r1_gemv_variants.txt).  MOM_GEMV_VARIANT=0 restores the old shape.
+  if (!is_bf16) return last_token_pair<false, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
+  if (gemv::env_or("MOM_GEMV_VARIANT", 1) == 0)
+    return last_token_pair<true, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
+  return last_token_pair<true, 2, 2, 4, 2, 4, 2>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
 }
 
 size_t lm_head_partials(int num_sms) { return static_cast<size_t>(num_sms) * 4; }

@@ -46,3 +46,36 @@ def test_knobs_are_bit_neutral(cuda_device):
                 os.environ[k] = v
     for knob, o in zip(KNOBS, outs):
         assert torch.equal(o, outs[0]), knob
+
+
+GEMV_KNOBS = [{}, {"MOM_GEMV_VARIANT": "0"}, {"MOM_GEMV_PDL": "0"}, {"MOM_GEMV_PREFETCH": "2"},
+              {"MOM_GEMV_VARIANT": "0", "MOM_GEMV_PDL": "0"}]
+GEMV_ALL = sorted({k for v in GEMV_KNOBS for k in v})
+
+
+@pytest.mark.parametrize("d,I", [(4096, 14336), (520, 1160)])
+def test_gemv_knobs_are_bit_neutral(cuda_device, d, I):
+    """Last-token GEMV shapes (rows per warp step, loads in flight, PDL, L2 prefetch) keep each
+    row's summation order: the output is bitwise identical for every setting."""
+    bf = torch.bfloat16
+    wg, wu, wd = synth.mlp_weights(d, I, 0, cuda_device, bf)
+    x = synth.hidden(1, d, cuda_device, bf)[0]
+    old = {k: os.environ.get(k) for k in GEMV_ALL}
+    outs = []
+    try:
+        for knob in GEMV_KNOBS:
+            for k in GEMV_ALL:
+                os.environ.pop(k, None)
+            os.environ.update(knob)
+            y = torch.empty_like(x)
+            _mom.mlp_last_token(x, x, wg, wu, wd, y)
+            torch.cuda.synchronize()
+            outs.append(y)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    for knob, y in zip(GEMV_KNOBS, outs):
+        assert torch.equal(y, outs[0]), knob

@@ -19,7 +19,10 @@ y = torch.empty(d, dtype=bf, device=dev)
 logits = torch.empty(V, dtype=torch.float32, device=dev)
 am = torch.empty(1, dtype=torch.int32, device=dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
+try:
+    peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
+except OSError:
+    peak = 6650.0  # B200_PROFILING.md fallback
 hot = os.environ.get("HOT", "0") == "1"
 if hot:
     xs = synth.hidden(w.C, d, dev, bf)
