@@ -133,6 +133,18 @@ class ClockSampler:
         fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
         return fn(self.h)
 
+    def _power_w(self):
+        """Instantaneous board power (NVML_FI_DEV_POWER_INSTANT); nvmlDeviceGetPowerUsage is a
+        1-s average on this GPU and under-reads a sub-second timed region."""
+        nv = self.nv
+        try:
+            fv = nv.nvmlDeviceGetFieldValues(self.h, [nv.NVML_FI_DEV_POWER_INSTANT])[0]
+            if fv.nvmlReturn == 0:
+                return fv.value.uiVal / 1000.0
+        except Exception:
+            pass
+        return nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+
     def _run(self):
         while not self._stop.is_set():
             try:
@@ -141,7 +153,7 @@ class ClockSampler:
                 for bit, name in self.REASONS.items():
                     if r & bit:
                         self.reasons.add(name)
-                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                self.power.append(self._power_w())
             except Exception:
                 pass
             time.sleep(self.period)
@@ -162,7 +174,8 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml-unavailable"]}
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples),
-                "power_w_max": max(self.power) if self.power else None}
+                "power_w_max": max(self.power) if self.power else None,
+                "power_w_median": statistics.median(self.power) if self.power else None}
 
 
 # ----------------------------------------------------------------------------- workload
