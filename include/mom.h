@@ -35,7 +35,8 @@
  *               MOM_GATHER_FORWARD (1: f1 rows of mini-sequence i-1 forwarded during i),
  *               MOM_GEMV_PDL (1), MOM_GEMV_VARIANT (1: down GEMV with 4 loads in flight per
  *               row at 2 blocks/SM; 0: the earlier 2 at 4/SM), MOM_MLP_PDL (1: programmatic dependent launch between the
- *               tcgen05 MLP launches of one call), MOM_NB_B (phase-B tile width; default: chosen per shape for
+ *               tcgen05 MLP launches of one call), MOM_HALF_TAIL (1: phase A's last partial wave as
+ *               half-width tiles when it fills <= half the clusters), MOM_NB_B (phase-B tile width; default: chosen per shape for
  *               wave quantisation).  None changes results: outputs are bitwise identical.
  *   Alignment   Device pointers must be 16-byte aligned and row pitches (hidden*w,
  *               intermediate*w, w = element bytes) multiples of 16 bytes (TMA rule).

@@ -270,11 +270,17 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
   // the power-capped B200 that energy costs more clock than the tail (energy sweep, round 1).
   const bool fused = env_int("MOM_FUSED", 0) != 0;
   const bool mlp_pdl = env_int("MOM_MLP_PDL", 1) != 0;
-  CUtensorMap tm_wg, tm_wu, tm_wd;
+  // phase-A wave tail as half-width tiles (bitwise neutral: same K order per output element)
+  const bool half_tail = env_int("MOM_HALF_TAIL", 1) != 0;
+  CUtensorMap tm_wg, tm_wu, tm_wd, tm_wg_h, tm_wu_h;
   mom_status_t st;
   if (dt == MOM_BF16) {
     if ((st = make_tmap(&tm_wg, w_gate, intermediate, hidden, "w_gate")) != MOM_OK) return st;
     if ((st = make_tmap(&tm_wu, w_up, intermediate, hidden, "w_up")) != MOM_OK) return st;
+    if (half_tail) {
+      if ((st = make_tmap(&tm_wg_h, w_gate, intermediate, hidden, "w_gate", 64)) != MOM_OK) return st;
+      if ((st = make_tmap(&tm_wu_h, w_up, intermediate, hidden, "w_up", 64)) != MOM_OK) return st;
+    }
   }
   uint32_t wd_box = 0;  // W_down map is (re)encoded when the phase-B tile width changes
   for (int64_t i = 0; i < M; ++i) {  // Alg. 1: for i = 1..M (sequential on `stream`)
@@ -323,6 +329,8 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     if ((st = make_tmap(&tm_h, h, rows, intermediate, "h_i")) != MOM_OK) return st;
     mom::TcMlpArgs a{};
     a.tm_x = &tm_x; a.tm_wg = &tm_wg; a.tm_wu = &tm_wu; a.tm_h = &tm_h; a.tm_wd = &tm_wd;
+    a.tm_wg_h = half_tail ? &tm_wg_h : nullptr;
+    a.tm_wu_h = half_tail ? &tm_wu_h : nullptr;
     a.rows = (uint32_t)rows; a.d = (uint32_t)hidden; a.I = (uint32_t)intermediate;
     a.h = h; a.out = static_cast<__nv_bfloat16 *>(oi); a.residual = static_cast<const __nv_bfloat16 *>(ri);
     a.cta_group = cta_group; a.policy = policy; a.num_sms = num_sms;

@@ -17,6 +17,8 @@ struct TcMlpArgs {
   const CUtensorMap *tm_wu;  // W_up [I, d]     (phase A B half 1)
   const CUtensorMap *tm_h;   // H_i [C_i, I]    (phase B operand A)
   const CUtensorMap *tm_wd;  // W_down [d, I]   (phase B B halves)
+  const CUtensorMap *tm_wg_h;  // W_gate / W_up with a 64-row box: phase-A half-width tail tiles
+  const CUtensorMap *tm_wu_h;  //   (null: no half tiles)
   uint32_t rows;             // C_i
   uint32_t d, I;
   __nv_bfloat16 *h;          // H_i (workspace)

@@ -78,6 +78,7 @@ struct Maps {
   CUtensorMap wu;  // B half 1 of phase A: W_up [I, d]
   CUtensorMap h;   // A of phase B: H_i [C_i, I]
   CUtensorMap wd;  // B halves of phase B: W_down [d, I]
+  CUtensorMap wg_h, wu_h;  // phase A half-width tail tiles: W_gate / W_up, 64-row boxes
 };
 
 struct Params {
@@ -88,6 +89,10 @@ struct Params {
   uint32_t nb;           // phase-B tile width (UMMA N, multiple of 32, <= 256), chosen for wave quantisation
   uint32_t group_m;      // raster: row blocks per group (N iterates inside a group)
   uint32_t policy;       // TMA L2 policy: 0 reuse-aware (default), 1 all evict_normal, 2 A evict_first
+  // Phase-A wave-tail split (MODE_A): tiles [0, n_full) are the usual 128-column tiles; the R tiles
+  // that would form the last, partial wave are instead 2R half-width (64-column) tiles, so the last
+  // wave takes half a tile time on up to 2R clusters (2R <= clusters).  n_half = 2R (0 = off).
+  uint32_t n_full, n_half;
   __nv_bfloat16 *h;              // phase A output H_i [rows, I]
   __nv_bfloat16 *out;            // phase B output rows [rows, d]
   const __nv_bfloat16 *residual; // phase B residual, may be null
@@ -105,7 +110,9 @@ struct Params {
 
 struct Tile {
   uint32_t m, n;
-  bool a;  // phase A tile
+  bool a;       // phase A tile
+  uint32_t c0;  // phase A: first H column (= first W_gate/W_up row) of the tile
+  uint32_t hw;  // phase A: H columns of the tile (BHALF, or BHALF / 2 for a tail half tile)
 };
 
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -114,6 +121,14 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 template <int MODE>
 __device__ __forceinline__ Tile decode_tile(uint32_t t, const Params &p) {
   Tile tl;
+  uint32_t half = 0;
+  bool is_half = false;
+  if (MODE == MODE_A && t >= p.n_full) {  // tail half tile: the same raster slot as full tile n_full + h/2
+    const uint32_t h = t - p.n_full;
+    t = p.n_full + h / 2;
+    half = h & 1u;
+    is_half = true;
+  }
   const uint32_t G = p.group_m;
   if constexpr (MODE == MODE_FUSED) {
     // Lagged order A0, (A1, B0), (A2, B1), ..., (A_{ng-1}, B_{ng-2}), B_{ng-1}: the phase-B tiles
@@ -165,12 +180,15 @@ __device__ __forceinline__ Tile decode_tile(uint32_t t, const Params &p) {
     tl.n = local / gm;
     tl.a = MODE == MODE_A;
   }
+  tl.hw = is_half ? BHALF / 2 : BHALF;
+  tl.c0 = tl.n * BHALF + half * (BHALF / 2);
   return tl;
 }
 
 template <int MODE>
 __host__ __device__ __forceinline__ uint32_t num_tiles_of(const Params &p) {
-  return MODE == MODE_A ? p.m_tiles * p.nA : MODE == MODE_B ? p.m_tiles * p.nB : p.m_tiles * (p.nA + p.nB);
+  return MODE == MODE_A ? (p.n_half ? p.n_full + p.n_half : p.m_tiles * p.nA)
+                        : MODE == MODE_B ? p.m_tiles * p.nB : p.m_tiles * (p.nA + p.nB);
 }
 
 __device__ __forceinline__ float silu_mul(float g, float u) {
@@ -188,15 +206,17 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 }
 
 // Phase A epilogue for one tile: H[row, col0 + j] = bf16(silu(g_j * rs) * (u_j * rs)), j < 128.
-__device__ __forceinline__ void epilogue_a(const Params &p, uint32_t taddr, uint32_t row, bool row_ok, uint32_t col0) {
+// hw = H columns of the tile (gate accumulators at TMEM columns [0, hw), up at [hw, 2 hw)).
+__device__ __forceinline__ void epilogue_a(const Params &p, uint32_t taddr, uint32_t row, bool row_ok, uint32_t col0,
+                                           uint32_t hw) {
   __nv_bfloat16 *orow = p.h + static_cast<size_t>(row) * p.I + col0;
   // folded RMSNorm (f3): gate/up of row r are scaled by r's 1/rms before the SiLU
   const float rs = (p.row_scale != nullptr && row_ok) ? p.row_scale[row] : 1.0f;
 #pragma unroll 1
-  for (uint32_t c = 0; c < BHALF / 32; ++c) {
+  for (uint32_t c = 0; c < hw / 32; ++c) {
     uint32_t g[32], u[32];
     ptx::tmem_ld_32x32b_x32(taddr + c * 32, g);
-    ptx::tmem_ld_32x32b_x32(taddr + BHALF + c * 32, u);
+    ptx::tmem_ld_32x32b_x32(taddr + hw + c * 32, u);
     ptx::tmem_ld_wait();
     if (p.row_scale != nullptr) {
 #pragma unroll
@@ -227,7 +247,7 @@ __device__ __forceinline__ void epilogue_a(const Params &p, uint32_t taddr, uint
 // Phase A epilogue, coalesced variant: 64 H columns (128 B per row) at a time through the same
 // per-warp 32 x 128 B XOR-swizzled stage as phase B, stored as full 128-B row segments.
 __device__ __forceinline__ void epilogue_a_coalesced(const Params &p, uint32_t taddr, uint32_t row0_warp,
-                                                     uint32_t col0, uint8_t *stage) {
+                                                     uint32_t col0, uint32_t hw, uint8_t *stage) {
   const uint32_t lane = ptx::lane_id();
   const uint32_t row = row0_warp + lane;
   const uint32_t sbase = ptx::smem_u32(stage);
@@ -235,12 +255,12 @@ __device__ __forceinline__ void epilogue_a_coalesced(const Params &p, uint32_t t
   const uint32_t cr = lane >> 3, cv = lane & 7;
   const float rs = (p.row_scale != nullptr && row < p.rows) ? p.row_scale[row] : 1.0f;
 #pragma unroll 1
-  for (uint32_t c = 0; c < BHALF / 64; ++c) {
+  for (uint32_t c = 0; c < hw / 64; ++c) {
 #pragma unroll
     for (uint32_t half = 0; half < 2; ++half) {  // 32 columns of g and u at a time (register budget)
       uint32_t g[32], u[32];
       ptx::tmem_ld_32x32b_x32(taddr + c * 64 + half * 32, g);
-      ptx::tmem_ld_32x32b_x32(taddr + BHALF + c * 64 + half * 32, u);
+      ptx::tmem_ld_32x32b_x32(taddr + hw + c * 64 + half * 32, u);
       ptx::tmem_ld_wait();
 #pragma unroll
       for (uint32_t v = 0; v < 4; ++v) {
@@ -437,9 +457,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           while (ld_acquire_gpu(cnt) < p.nA) __nanosleep(128);
           fence_proxy_async_global();
         }
+        const bool half_a = tl.a && tl.hw < BHALF;
         const CUtensorMap *ta = tl.a ? &maps.x : &maps.h;
-        const CUtensorMap *tb0 = tl.a ? &maps.wg : &maps.wd;
-        const CUtensorMap *tb1 = tl.a ? &maps.wu : &maps.wd;
+        const CUtensorMap *tb0 = tl.a ? (half_a ? &maps.wg_h : &maps.wg) : &maps.wd;
+        const CUtensorMap *tb1 = tl.a ? (half_a ? &maps.wu_h : &maps.wu) : &maps.wd;
         uint64_t pol_a, pol_b;
         switch (p.policy) {
           case 1: pol_a = pol_norm; pol_b = pol_norm; break;                          // all normal
@@ -450,10 +471,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           default: pol_a = tl.a ? pol_keep : pol_norm; pol_b = tl.a ? pol_norm : pol_keep; break;
         }
         const int32_t a_row = static_cast<int32_t>(tl.m * BM * CG + rank * BM);
-        const int32_t b_row0 = static_cast<int32_t>(tl.a ? tl.n * BHALF : tl.n * p.nb);
+        const int32_t b_row0 = static_cast<int32_t>(tl.a ? tl.c0 : tl.n * p.nb);
         const int32_t b_off1 = tl.a ? 0 : static_cast<int32_t>(p.nb / 2);  // row offset of B half 1
         // bytes landing per stage: phase B's B halves are nb/2 rows (nb < 256 for some shapes)
-        const uint32_t bhalf_bytes = tl.a ? BHALF_BYTES : (p.nb / 2) * BK * 2;
+        const uint32_t bhalf_bytes = tl.a ? tl.hw * BK * 2 : (p.nb / 2) * BK * 2;
         const uint32_t tx_bytes = (A_BYTES + (CG == 1 ? 2 : 1) * bhalf_bytes) * CG;
         const uint32_t num_kb = tl.a ? kbA : kbB;
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
@@ -488,13 +509,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ======================= MMA issuer (leader CTA, one thread) =======================
     if (leader && lane == 0) {
       constexpr uint32_t idesc_a = ptx::idesc_bf16_f32(BM * CG, UMMA_N);
+      constexpr uint32_t idesc_a_half = ptx::idesc_bf16_f32(BM * CG, UMMA_N / 2);
       const uint32_t idesc_b = ptx::idesc_bf16_f32(BM * CG, p.nb);
       uint32_t stage = 0, phase = 0;
       uint32_t acc = 0, acc_phase = 0;
       for (uint32_t t = cluster_id; t < num_tiles; t += num_clusters) {
         const Tile tl = decode_tile<MODE>(t, p);
         const uint32_t num_kb = tl.a ? kbA : kbB;
-        const uint32_t idesc = tl.a ? idesc_a : idesc_b;
+        const uint32_t idesc = tl.a ? (tl.hw < BHALF ? idesc_a_half : idesc_a) : idesc_b;
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * ACC_COLS;
@@ -532,9 +554,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool row_ok = row < p.rows;
       const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * ACC_COLS;
       if (tl.a && p.coalesced_a)
-        epilogue_a_coalesced(p, taddr, row - lane, tl.n * BHALF, epi_stage + q * 32 * 128);
+        epilogue_a_coalesced(p, taddr, row - lane, tl.c0, tl.hw, epi_stage + q * 32 * 128);
       else if (tl.a)
-        epilogue_a(p, taddr, row, row_ok, tl.n * BHALF);
+        epilogue_a(p, taddr, row, row_ok, tl.c0, tl.hw);
       else
         epilogue_b(p, taddr, row - lane, tl.n * p.nb, epi_stage + q * 32 * 128);
       // release the accumulator to the MMA issuer
@@ -631,6 +653,8 @@ static cudaError_t launch_mode(const TcMlpArgs &a, cudaStream_t stream) {
   maps.wu = *a.tm_wu;
   maps.h = *a.tm_h;
   maps.wd = *a.tm_wd;
+  maps.wg_h = a.tm_wg_h ? *a.tm_wg_h : *a.tm_wg;
+  maps.wu_h = a.tm_wu_h ? *a.tm_wu_h : *a.tm_wu;
   Params p{};
   p.rows = a.rows;
   p.d = a.d;
@@ -644,6 +668,20 @@ static cudaError_t launch_mode(const TcMlpArgs &a, cudaStream_t stream) {
   if (g > p.m_tiles) g = p.m_tiles;
   p.group_m = g;
   p.policy = a.policy;
+  // phase-A wave tail: T tiles on `clusters` persistent clusters leave R = T mod clusters tiles for
+  // a last partial wave; when 2R <= clusters they run as 2R half-width tiles (half a tile time)
+  p.n_full = num_tiles_of<MODE>(p);
+  p.n_half = 0;
+  if (MODE == MODE_A && a.tm_wg_h && a.tm_wu_h) {
+    const uint32_t T = p.m_tiles * p.nA;
+    uint32_t clusters = static_cast<uint32_t>(a.num_sms) / a.cta_group;
+    if (clusters > T) clusters = T;
+    const uint32_t R = clusters ? T % clusters : 0;
+    if (R > 0 && 2 * R <= clusters) {
+      p.n_full = T - R;
+      p.n_half = 2 * R;
+    }
+  }
   p.h = a.h;
   p.out = a.out;
   p.residual = a.residual;

@@ -17,7 +17,7 @@ KNOBS = [{}, {"MOM_CTA_GROUP": "1"}, {"MOM_GROUP_M_A": "1"}, {"MOM_GROUP_M_A": "
          {"MOM_FUSED": "1", "MOM_GROUP_M_A": "2"}, {"MOM_EPI_A_COALESCED": "0"}, {"MOM_NB_B": "256"},
          {"MOM_NB_B": "224"}, {"MOM_NB_B": "160"}, {"MOM_NB_B": "128"}, {"MOM_NB_B": "96"},
          {"MOM_NB_B": "224", "MOM_CTA_GROUP": "1"}, {"MOM_NB_B": "192", "MOM_FUSED": "1"}, {"MOM_MLP_PDL": "0"},
-         {"MOM_MLP_PDL": "0", "MOM_CTA_GROUP": "1"}]
+         {"MOM_MLP_PDL": "0", "MOM_CTA_GROUP": "1"}, {"MOM_HALF_TAIL": "0"}, {"MOM_HALF_TAIL": "0", "MOM_CTA_GROUP": "1"}]
 ALL = sorted({k for v in KNOBS for k in v})
 
 
@@ -79,3 +79,37 @@ def test_gemv_knobs_are_bit_neutral(cuda_device, d, I):
                 os.environ[k] = v
     for knob, y in zip(GEMV_KNOBS, outs):
         assert torch.equal(y, outs[0]), knob
+
+
+@pytest.mark.parametrize("cg", ["2", "1"])
+def test_half_width_tail_tiles(cuda_device, cg):
+    """Phase A's last partial wave runs as half-width (64-column) tiles when it fills at most half
+    of the clusters (S=2000, C=600, I=4096: 96 tiles on 74 pairs -> 22 tiles become 44 halves; 1-CTA:
+    160 on 148 -> 12 -> 24).  Same K order per element: bitwise equal to full tiles, and to the oracle."""
+    import oracle
+    from tests.parity import TOL_BF16, check_close
+    S, d, I, C = 2000, 512, 4096, 600
+    bf = torch.bfloat16
+    wg, wu, wd = synth.mlp_weights(d, I, 0, cuda_device, bf)
+    x = synth.hidden(S, d, cuda_device, bf)
+    old = {k: os.environ.get(k) for k in ("MOM_HALF_TAIL", "MOM_CTA_GROUP")}
+    outs = []
+    try:
+        os.environ["MOM_CTA_GROUP"] = cg
+        for ht in ("1", "0"):
+            os.environ["MOM_HALF_TAIL"] = ht
+            o = torch.empty_like(x)
+            _mom.mlp_minseq_fwd(x, x, wg, wu, wd, o, C)
+            torch.cuda.synchronize()
+            outs.append(o)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert torch.equal(outs[0], outs[1])
+    rows = [0, 599, 600, 1199, 1200, 1799, 1800, 1999] + list(range(3, S, 97))
+    xc = x.cpu()
+    ref = oracle.mlp_rows(xc, xc, wg.cpu(), wu.cpu(), wd.cpu(), rows)
+    check_close(outs[0].cpu()[rows], ref, TOL_BF16, "half-width tail tiles")
