@@ -1,0 +1,26 @@
+"""Small tcgen05 MLP calls for compute-sanitizer: ragged mini-sequences with phase-A half-width tail
+tiles (S=2000, C=600, I=4096), both CTA-group modes, plus the last-token GEMVs and the LM head."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import synth
+from paper_2504_12526_b200 import _mom
+
+dev = torch.device("cuda:0")
+bf = torch.bfloat16
+S, d, I, C = 2000, 512, 4096, 600
+wg, wu, wd = synth.mlp_weights(d, I, 0, dev, bf)
+x = synth.hidden(S, d, dev, bf)
+for cg in ("2", "1"):
+    os.environ["MOM_CTA_GROUP"] = cg
+    out = torch.empty_like(x)
+    _mom.mlp_minseq_fwd(x, x, wg, wu, wd, out, C)
+    torch.cuda.synchronize()
+y = torch.empty(d, dtype=bf, device=dev)
+_mom.mlp_last_token(out[-1], out[-1], wg, wu, wd, y)
+wh = synth.head_weight(1000, d, dev, bf)
+logits = torch.empty(1000, dtype=torch.float32, device=dev)
+am = torch.empty(1, dtype=torch.int32, device=dev)
+_mom.lm_head_last(y, synth.norm_gain(d, dev, bf), 1e-5, wh, logits, am)
+torch.cuda.synchronize()
+print("sanitize case OK", float(out.float().abs().mean()), int(am.item()))
