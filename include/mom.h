@@ -38,6 +38,8 @@
  *               tcgen05 MLP launches of one call), MOM_HALF_TAIL (1: phase A's last partial wave as
  *               half-width tiles when it fills <= half the clusters), MOM_NB_B (phase-B tile width; default: chosen per shape for
  *               wave quantisation).  None changes results: outputs are bitwise identical.
+ *               Numerics knob: MOM_FAST_SILU (1: the phase-A SiLU quotient by rcp.approx, <= 2 fp32
+ *               ulp; 0: IEEE division, whose per-element slow-path branch serialises the epilogue).
  *   Alignment   Device pointers must be 16-byte aligned and row pitches (hidden*w,
  *               intermediate*w, w = element bytes) multiples of 16 bytes (TMA rule).
  *   Dtypes      MOM_BF16: bf16 storage, fp32 accumulation, fp32 SiLU, one RNE rounding of

@@ -27,6 +27,7 @@ struct TcMlpArgs {
   const float *row_scale;    // folded RMSNorm 1/rms per row (phase A), or null
   uint32_t *ready;           // fused mode: mlp_tc_ready_counters(rows) zeroed counters
   uint32_t coalesced_a;      // phase-A epilogue via the smem stage (coalesced H stores)
+  uint32_t fast_silu;        // phase-A epilogue SiLU quotient by rcp.approx (MOM_FAST_SILU, default 1)
   uint32_t n_peers;          // f1: number of peer destinations (<= kMaxPeers)
   __nv_bfloat16 *peer_out[kMaxPeers];  // f1: peer gathered buffers at this mini-sequence's rows
   const __nv_bfloat16 *fwd_src;        // f1: previous mini-sequence's output rows to forward (or null)

@@ -99,6 +99,7 @@ struct Params {
   const float *row_scale;        // phase A: folded-RMSNorm 1/rms per row, or null
   uint32_t *ready;               // MODE_FUSED: per (row block, CTA rank) count of finished phase-A tiles
   uint32_t coalesced_a;          // phase-A epilogue through the smem stage (128-B row segments)
+  uint32_t fast_silu;            // phase-A epilogue: quotient of the SiLU by rcp.approx (no branch)
   uint32_t n_peers;              // f1: extra destinations of the phase-B output rows
   __nv_bfloat16 *peer_out[kMaxPeers];  // f1: peers' gathered buffers, offset like `out`
   // f1 forwarding (warps 2-3): rows [0, fwd_rows) of fwd_src (the previous mini-sequence's
@@ -191,8 +192,12 @@ __host__ __device__ __forceinline__ uint32_t num_tiles_of(const Params &p) {
                         : MODE == MODE_B ? p.m_tiles * p.nB : p.m_tiles * (p.nA + p.nB);
 }
 
+// Swish(g) * u = g * sigmoid(g) * u, fp32.  FAST: the quotient by rcp.approx (<= 2 ulp,
+// no slow-path branch) instead of IEEE division, whose per-element FCHK/branch region kept the
+// compiler from interleaving elements (the phase-A epilogue was latency-bound on it).
+template <bool FAST>
 __device__ __forceinline__ float silu_mul(float g, float u) {
-  // Swish(g) * u = g * sigmoid(g) * u, fp32
+  if constexpr (FAST) return __fdividef(g, 1.0f + __expf(-g)) * u;
   return g / (1.0f + __expf(-g)) * u;
 }
 
@@ -207,6 +212,7 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 
 // Phase A epilogue for one tile: H[row, col0 + j] = bf16(silu(g_j * rs) * (u_j * rs)), j < 128.
 // hw = H columns of the tile (gate accumulators at TMEM columns [0, hw), up at [hw, 2 hw)).
+template <bool FAST>
 __device__ __forceinline__ void epilogue_a(const Params &p, uint32_t taddr, uint32_t row, bool row_ok, uint32_t col0,
                                            uint32_t hw) {
   __nv_bfloat16 *orow = p.h + static_cast<size_t>(row) * p.I + col0;
@@ -228,8 +234,8 @@ __device__ __forceinline__ void epilogue_a(const Params &p, uint32_t taddr, uint
     uint32_t packed[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      float h0 = silu_mul(__uint_as_float(g[2 * i]), __uint_as_float(u[2 * i]));
-      float h1 = silu_mul(__uint_as_float(g[2 * i + 1]), __uint_as_float(u[2 * i + 1]));
+      float h0 = silu_mul<FAST>(__uint_as_float(g[2 * i]), __uint_as_float(u[2 * i]));
+      float h1 = silu_mul<FAST>(__uint_as_float(g[2 * i + 1]), __uint_as_float(u[2 * i + 1]));
       packed[i] = ptx::pack_bf16x2(h0, h1);
     }
     if (row_ok) {
@@ -246,6 +252,7 @@ __device__ __forceinline__ void epilogue_a(const Params &p, uint32_t taddr, uint
 
 // Phase A epilogue, coalesced variant: 64 H columns (128 B per row) at a time through the same
 // per-warp 32 x 128 B XOR-swizzled stage as phase B, stored as full 128-B row segments.
+template <bool FAST>
 __device__ __forceinline__ void epilogue_a_coalesced(const Params &p, uint32_t taddr, uint32_t row0_warp,
                                                      uint32_t col0, uint32_t hw, uint8_t *stage) {
   const uint32_t lane = ptx::lane_id();
@@ -272,7 +279,7 @@ __device__ __forceinline__ void epilogue_a_coalesced(const Params &p, uint32_t t
           if (p.row_scale != nullptr) {
             g0 *= rs; g1 *= rs; u0 *= rs; u1 *= rs;
           }
-          w[e] = ptx::pack_bf16x2(silu_mul(g0, u0), silu_mul(g1, u1));
+          w[e] = ptx::pack_bf16x2(silu_mul<FAST>(g0, u0), silu_mul<FAST>(g1, u1));
         }
         asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sw(lane, half * 4 + v)), "r"(w[0]), "r"(w[1]),
                      "r"(w[2]), "r"(w[3])
@@ -553,10 +560,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t row = tl.m * BM * CG + rank * BM + row_in_tile;
       const bool row_ok = row < p.rows;
       const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * ACC_COLS;
-      if (tl.a && p.coalesced_a)
-        epilogue_a_coalesced(p, taddr, row - lane, tl.c0, tl.hw, epi_stage + q * 32 * 128);
+      if (tl.a && p.coalesced_a && p.fast_silu)
+        epilogue_a_coalesced<true>(p, taddr, row - lane, tl.c0, tl.hw, epi_stage + q * 32 * 128);
+      else if (tl.a && p.coalesced_a)
+        epilogue_a_coalesced<false>(p, taddr, row - lane, tl.c0, tl.hw, epi_stage + q * 32 * 128);
+      else if (tl.a && p.fast_silu)
+        epilogue_a<true>(p, taddr, row, row_ok, tl.c0, tl.hw);
       else if (tl.a)
-        epilogue_a(p, taddr, row, row_ok, tl.c0, tl.hw);
+        epilogue_a<false>(p, taddr, row, row_ok, tl.c0, tl.hw);
       else
         epilogue_b(p, taddr, row - lane, tl.n * p.nb, epi_stage + q * 32 * 128);
       // release the accumulator to the MMA issuer
@@ -688,6 +699,7 @@ static cudaError_t launch_mode(const TcMlpArgs &a, cudaStream_t stream) {
   p.row_scale = a.row_scale;
   p.ready = a.ready;
   p.coalesced_a = a.coalesced_a;
+  p.fast_silu = a.fast_silu;
   p.fwd_src = a.fwd_src;
   p.fwd_rows = a.fwd_rows;
   p.n_fwd = a.fwd_src ? a.n_fwd : 0;

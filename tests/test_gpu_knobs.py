@@ -113,3 +113,30 @@ def test_half_width_tail_tiles(cuda_device, cg):
     xc = x.cpu()
     ref = oracle.mlp_rows(xc, xc, wg.cpu(), wu.cpu(), wd.cpu(), rows)
     check_close(outs[0].cpu()[rows], ref, TOL_BF16, "half-width tail tiles")
+
+
+@pytest.mark.parametrize("fast", ["1", "0"])
+def test_silu_quotient_variants_vs_oracle(cuda_device, fast):
+    """MOM_FAST_SILU: the phase-A SiLU quotient by rcp.approx (default) or IEEE division.  Not a
+    bit-neutral knob (<= 2 fp32 ulp before the bf16 rounding of H); both meet the oracle bar."""
+    import oracle
+    from tests.parity import TOL_BF16, check_close
+    S, d, I, C = 1500, 512, 1160, 700
+    bf = torch.bfloat16
+    wg, wu, wd = synth.mlp_weights(d, I, 0, cuda_device, bf)
+    x = synth.hidden(S, d, cuda_device, bf)
+    old = os.environ.get("MOM_FAST_SILU")
+    try:
+        os.environ["MOM_FAST_SILU"] = fast
+        o = torch.empty_like(x)
+        _mom.mlp_minseq_fwd(x, x, wg, wu, wd, o, C)
+        torch.cuda.synchronize()
+    finally:
+        if old is None:
+            os.environ.pop("MOM_FAST_SILU", None)
+        else:
+            os.environ["MOM_FAST_SILU"] = old
+    rows = [0, 699, 700, 1399, 1400, 1499] + list(range(5, S, 61))
+    xc = x.cpu()
+    check_close(o.cpu()[rows], oracle.mlp_rows(xc, xc, wg.cpu(), wu.cpu(), wd.cpu(), rows), TOL_BF16,
+                f"MOM_FAST_SILU={fast}")
