@@ -74,7 +74,7 @@ def parse_args():
 
 # ----------------------------------------------------------------------------- distributed
 # Test mode for the N > 1 code path on a one-GPU box: every rank on cuda:0, gloo instead of NCCL,
-# host barriers instead of mom_nccl_barrier, no e2e leg.  Never used for a reported number.
+# host barriers instead of mom_nccl_barrier, e2e only with the fused gather.  Never used for a reported number.
 SHARED_GPU = os.environ.get("MOM_BENCH_SHARED_GPU") == "1"
 
 
@@ -266,23 +266,25 @@ def run_step(wl, compute, copy, reload, launches, x_host=None, h2d=None, serial=
         # two device input buffers: this request's rows stream in (per mini-sequence) as soon as
         # the request two back is done with the buffer, i.e. while the previous request computes
         xd = wl.x_bufs[slot]
-        _mom.mlp_minseq_fwd_from_host(x_host, xd, xd, wg, wu, wd, wl.shard, wl.C, wl.ws, compute, h2d,
-                                      x_free=wl.ev_x_free[slot])
+        if wl.world > 1 and wl.peers:  # + a11 fused (f1), as in the device leg
+            _mom.mlp_minseq_fwd_from_host_gather(x_host, xd, xd, wg, wu, wd, wl.shard, wl.peers, wl.C, wl.ws,
+                                                 compute, h2d, x_free=wl.ev_x_free[slot])
+        else:
+            _mom.mlp_minseq_fwd_from_host(x_host, xd, xd, wg, wu, wd, wl.shard, wl.C, wl.ws, compute, h2d,
+                                          x_free=wl.ev_x_free[slot])
         wl.ev_x_free[slot].record(compute)
         # the previous request's reload shares the H2D direction: queue it behind this request's
         # input rows so it does not delay the mini-sequences waiting for them
         flush_reload(wl, h2d)
-        if wl.world > 1:
+        if wl.world > 1 and wl.peers:
+            barrier_after_gather(wl, compute)
+        elif wl.world > 1:
             _mom.allgather_rows(wl.out, wl.S, wl.comm, wl.rank, wl.world, compute)       # a11 (NCCL)
     elif wl.world > 1 and wl.peers:
         # a1-a4 + a11: the phase-B epilogue stores every output row to all peers (f1), then a
         # 1-element NCCL all-reduce orders everyone's peer stores before the next layer
         _mom.mlp_minseq_fwd_gather(wl.x, wl.x, wg, wu, wd, wl.shard, wl.peers, wl.C, wl.ws, compute)
-        if wl.comm is not None:
-            _mom.nccl_barrier(wl.comm, wl.barrier_scratch, compute)
-        else:  # SHARED_GPU test mode: host barrier
-            compute.synchronize()
-            dist.barrier()
+        barrier_after_gather(wl, compute)
     else:
         _mom.mlp_minseq_fwd(wl.x, wl.x, wg, wu, wd, wl.shard, wl.C, wl.ws, compute)     # a1-a4
         if wl.world > 1:
@@ -300,6 +302,17 @@ def run_step(wl, compute, copy, reload, launches, x_host=None, h2d=None, serial=
         flush_reload(wl, reload)
     if serial:
         compute.wait_event(wl.ev_reloaded[slot])
+
+
+def barrier_after_gather(wl, compute):
+    """Order every rank's peer stores before any rank's next layer: a 1-element NCCL all-reduce on
+    the compute stream (SHARED_GPU test mode: a host barrier)."""
+    from paper_2504_12526_b200 import _mom
+    if wl.comm is not None:
+        _mom.nccl_barrier(wl.comm, wl.barrier_scratch, compute)
+    else:
+        compute.synchronize()
+        dist.barrier()
 
 
 def flush_reload(wl, stream):
@@ -395,8 +408,8 @@ def run_mine(args):
             obj = [uid]
             dist.broadcast_object_list(obj, src=0)
             wl.comm = _mom.nccl_comm_init(world, obj[0], rank)
-        else:
-            args.no_e2e = True
+        elif args.gather != "fused":
+            args.no_e2e = True  # the NCCL all-gather needs one GPU per rank
         if args.gather == "fused":
             wl.map_peers()
     compute = torch.cuda.Stream(device)

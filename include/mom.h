@@ -253,6 +253,16 @@ mom_status_t mom_mlp_minseq_fwd_gather(const void *x, const void *residual, cons
                                        void *const *peer_out, int n_peers, int64_t S, int64_t hidden,
                                        int64_t intermediate, int64_t minseq_len, mom_dtype_t dt,
                                        void *workspace, size_t workspace_bytes, mom_stream_t stream);
+/* The end-to-end entry of token-sharded runs: mom_mlp_minseq_fwd_from_host (input streamed from
+ * pinned host memory per mini-sequence, optional x_free prefetch) whose output rows also go to
+ * the n_peers buffers as in mom_mlp_minseq_fwd_gather.  Arguments and errors as those two. */
+mom_status_t mom_mlp_minseq_fwd_from_host_gather(const void *x_host_pinned, void *x, const void *residual,
+                                                 const void *w_gate, const void *w_up, const void *w_down,
+                                                 void *out, void *const *peer_out, int n_peers, int64_t S,
+                                                 int64_t hidden, int64_t intermediate, int64_t minseq_len,
+                                                 mom_dtype_t dt, void *workspace, size_t workspace_bytes,
+                                                 mom_stream_t stream, mom_stream_t copy_stream,
+                                                 mom_event_t x_free);
 mom_status_t mom_ipc_get_handle(const void *dev_ptr, void *handle_out /* 64 B */, int64_t *offset_out);
 mom_status_t mom_ipc_open_handle(const void *handle /* 64 B */, int64_t offset, void **dev_ptr_out);
 mom_status_t mom_ipc_close(void *dev_ptr, int64_t offset);

@@ -46,6 +46,8 @@ SIGNATURES = {
     "mom_nccl_barrier": (_i32, [_p, _p, _p]),
     "mom_mlp_minseq_fwd_gather": (_i32, [_p, _p, _p, _p, _p, _p, _p, _i32, _i64, _i64, _i64, _i64, _i32, _p, _sz,
                                          _p]),
+    "mom_mlp_minseq_fwd_from_host_gather": (_i32, [_p, _p, _p, _p, _p, _p, _p, _p, _i32, _i64, _i64, _i64, _i64,
+                                                   _i32, _p, _sz, _p, _p, _p]),
     "mom_ipc_get_handle": (_i32, [_p, _p, ctypes.POINTER(ctypes.c_int64)]),
     "mom_ipc_open_handle": (_i32, [_p, _i64, ctypes.POINTER(ctypes.c_void_p)]),
     "mom_ipc_close": (_i32, [_p, _i64]),
@@ -316,6 +318,27 @@ def mlp_minseq_fwd_gather(x, residual, w_gate, w_up, w_down, out, peer_out, mins
     _check(lib().mom_mlp_minseq_fwd_gather(_ptr(x), _ptr(residual), _ptr(w_gate), _ptr(w_up), _ptr(w_down), _ptr(out),
                                            arr, len(peers), S, hidden, I, minseq_len, dt, _ptr(workspace),
                                            workspace.numel() * workspace.element_size(), _stream(stream)))
+    return out
+
+
+def mlp_minseq_fwd_from_host_gather(x_host, x, residual, w_gate, w_up, w_down, out, peer_out, minseq_len: int,
+                                    workspace=None, stream=None, copy_stream=None, x_free=None):
+    """End-to-end entry of token-sharded runs: mlp_minseq_fwd_from_host whose output rows also go
+    to every peer buffer (as mlp_minseq_fwd_gather)."""
+    S, hidden = x.shape
+    I = w_gate.shape[0]
+    dt = _dt(x)
+    if workspace is None:
+        nbytes = lib().mom_mlp_minseq_workspace_bytes(S, hidden, I, minseq_len, dt)
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    if copy_stream is None:
+        raise ValueError("copy_stream is required")
+    peers = [_ptr(p) for p in peer_out]
+    arr = (ctypes.c_void_p * max(1, len(peers)))(*peers)
+    _check(lib().mom_mlp_minseq_fwd_from_host_gather(
+        _ptr(x_host), _ptr(x), _ptr(residual), _ptr(w_gate), _ptr(w_up), _ptr(w_down), _ptr(out), arr, len(peers),
+        S, hidden, I, minseq_len, dt, _ptr(workspace), workspace.numel() * workspace.element_size(), _stream(stream),
+        _stream(copy_stream), _event_handle(x_free)))
     return out
 
 

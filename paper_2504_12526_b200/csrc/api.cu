@@ -483,36 +483,69 @@ mom_status_t mom_ipc_close(void *dev_ptr, int64_t offset) {
   return MOM_OK;
 }
 
+}  // extern "C"
+
+namespace {
+mom_status_t from_host_impl(const char *who, const void *x_host_pinned, void *x, const void *residual,
+                            const void *w_gate, const void *w_up, const void *w_down, void *out,
+                            void *const *peer_out, int n_peers, int64_t S, int64_t hidden, int64_t intermediate,
+                            int64_t C, mom_dtype_t dt, void *workspace, size_t workspace_bytes, mom_stream_t stream,
+                            mom_stream_t copy_stream, mom_event_t x_free) {
+  g_err[0] = 0;
+  if (!x_host_pinned) return fail(MOM_ERR_INVALID_ARG, "%s: null host pointer", who);
+  mom_status_t st = validate_minseq(who, x, residual, w_gate, w_up, w_down, out, S, hidden, intermediate, C, dt,
+                                    workspace, workspace_bytes);
+  if (st != MOM_OK) return st;
+  if (n_peers < 0 || n_peers > static_cast<int>(mom::kMaxPeers) || (n_peers > 0 && !peer_out))
+    return fail(MOM_ERR_INVALID_ARG, "%s: 0 <= n_peers <= %u", who, mom::kMaxPeers);
+  for (int k = 0; k < n_peers; ++k)
+    if (!peer_out[k] || !aligned16(peer_out[k]))
+      return fail(MOM_ERR_INVALID_ARG, "%s: peer %d pointer null or misaligned", who, k);
+  if (dt != MOM_BF16 && n_peers > 0) return fail(MOM_ERR_UNSUPPORTED, "%s: peer stores are bf16 only", who);
+  if ((st = check_pinned(x_host_pinned, who)) != MOM_OK) return st;
+  if (copy_stream == stream) return fail(MOM_ERR_INVALID_ARG, "%s: copy_stream must differ from stream", who);
+  cudaStream_t s = static_cast<cudaStream_t>(stream), cp = static_cast<cudaStream_t>(copy_stream);
+  cudaError_t e;
+  if (x_free) {
+    // the caller names the point after which x is free (double-buffered inputs: prefetch)
+    e = cudaStreamWaitEvent(cp, static_cast<cudaEvent_t>(x_free), 0);
+    if (e != cudaSuccess) return cuda_fail(e, "x_free ordering");
+  } else {
+    // the copy stream must not start writing x before earlier work on `stream` is done with it
+    cudaEvent_t ready;
+    e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "event create");
+    e = cudaEventRecord(ready, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cp, ready, 0);
+    cudaEventDestroy(ready);
+    if (e != cudaSuccess) return cuda_fail(e, "stream ordering");
+  }
+  return run_minseq(x, residual, w_gate, w_up, w_down, out, S, hidden, intermediate, C, dt, workspace, s,
+                    x_host_pinned, cp, nullptr, peer_out, n_peers);
+}
+}  // namespace
+
+extern "C" {
+
 mom_status_t mom_mlp_minseq_fwd_from_host(const void *x_host_pinned, void *x, const void *residual,
                                           const void *w_gate, const void *w_up, const void *w_down, void *out,
                                           int64_t S, int64_t hidden, int64_t intermediate, int64_t C,
                                           mom_dtype_t dt, void *workspace, size_t workspace_bytes,
                                           mom_stream_t stream, mom_stream_t copy_stream, mom_event_t x_free) {
-  g_err[0] = 0;
-  if (!x_host_pinned) return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd_from_host: null host pointer");
-  mom_status_t st = validate_minseq("mom_mlp_minseq_fwd_from_host", x, residual, w_gate, w_up, w_down, out, S,
-                                    hidden, intermediate, C, dt, workspace, workspace_bytes);
-  if (st != MOM_OK) return st;
-  if ((st = check_pinned(x_host_pinned, "mom_mlp_minseq_fwd_from_host")) != MOM_OK) return st;
-  if (copy_stream == stream) return fail(MOM_ERR_INVALID_ARG, "mom_mlp_minseq_fwd_from_host: copy_stream must differ from stream");
-  cudaStream_t s = static_cast<cudaStream_t>(stream), cp = static_cast<cudaStream_t>(copy_stream);
-  if (x_free) {
-    // the caller names the point after which x is free (double-buffered inputs: prefetch)
-    cudaError_t e = cudaStreamWaitEvent(cp, static_cast<cudaEvent_t>(x_free), 0);
-    if (e != cudaSuccess) return cuda_fail(e, "x_free ordering");
-    return run_minseq(x, residual, w_gate, w_up, w_down, out, S, hidden, intermediate, C, dt, workspace, s,
-                      x_host_pinned, cp);
-  }
-  // the copy stream must not start writing x before earlier work on `stream` is done with it
-  cudaEvent_t ready;
-  cudaError_t e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
-  if (e != cudaSuccess) return cuda_fail(e, "event create");
-  e = cudaEventRecord(ready, s);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(cp, ready, 0);
-  cudaEventDestroy(ready);
-  if (e != cudaSuccess) return cuda_fail(e, "stream ordering");
-  return run_minseq(x, residual, w_gate, w_up, w_down, out, S, hidden, intermediate, C, dt, workspace, s,
-                    x_host_pinned, cp);
+  return from_host_impl("mom_mlp_minseq_fwd_from_host", x_host_pinned, x, residual, w_gate, w_up, w_down, out,
+                        nullptr, 0, S, hidden, intermediate, C, dt, workspace, workspace_bytes, stream, copy_stream,
+                        x_free);
+}
+
+mom_status_t mom_mlp_minseq_fwd_from_host_gather(const void *x_host_pinned, void *x, const void *residual,
+                                                 const void *w_gate, const void *w_up, const void *w_down,
+                                                 void *out, void *const *peer_out, int n_peers, int64_t S,
+                                                 int64_t hidden, int64_t intermediate, int64_t C, mom_dtype_t dt,
+                                                 void *workspace, size_t workspace_bytes, mom_stream_t stream,
+                                                 mom_stream_t copy_stream, mom_event_t x_free) {
+  return from_host_impl("mom_mlp_minseq_fwd_from_host_gather", x_host_pinned, x, residual, w_gate, w_up, w_down,
+                        out, peer_out, n_peers, S, hidden, intermediate, C, dt, workspace, workspace_bytes, stream,
+                        copy_stream, x_free);
 }
 
 mom_status_t mom_fold_norm_gain(const void *w, const void *norm_gain, void *w_folded, int64_t rows, int64_t cols,

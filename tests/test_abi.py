@@ -116,6 +116,13 @@ def test_new_entry_points_reject_bad_arguments(lib):
     # from_host: null host pointer
     assert lib.mom_mlp_minseq_fwd_from_host(None, 16, None, 32, 48, 64, 80, 4, 8, 16, 2, 0, 96, 1 << 20, None,
                                             None, None) == E
+    # from_host + gather: null host pointer, too many peers, null peer
+    assert lib.mom_mlp_minseq_fwd_from_host_gather(None, 16, None, 32, 48, 64, 80, peers, 1, 4, 8, 16, 2, 0, 96,
+                                                   1 << 20, None, None, None) == E
+    assert lib.mom_mlp_minseq_fwd_from_host_gather(112, 16, None, 32, 48, 64, 80, peers, 8, 4, 8, 16, 2, 0, 96,
+                                                   1 << 20, None, None, None) == E
+    assert lib.mom_mlp_minseq_fwd_from_host_gather(112, 16, None, 32, 48, 64, 80, peers, 1, 4, 8, 16, 2, 0, 96,
+                                                   1 << 20, None, None, None) == E
     # folded norm: fp32 unsupported, bad eps, misaligned
     assert lib.mom_fold_norm_gain(16, 32, 48, 4, 8, _mom.MOM_F32, None) == U
     assert lib.mom_fold_norm_gain(16, 32, 48, 4, 6, _mom.MOM_BF16, None) == E

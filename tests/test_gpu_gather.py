@@ -54,6 +54,37 @@ def test_gather_into_local_peer_buffers(cuda_device, fused, cg, fwd):
                                                                                   sentinel[(rank + 1) * S:])
 
 
+@pytest.mark.parametrize("fwd", ["1", "0"])
+def test_from_host_gather_into_local_peer_buffers(cuda_device, fwd):
+    """The end-to-end entry of token-sharded runs: input streamed from pinned host memory per
+    mini-sequence (x_free prefetch event), output rows stored to every peer buffer too."""
+    os.environ["MOM_GATHER_FORWARD"] = fwd
+    S, d, I, C, world, rank = 700, 512, 1024, 256, 3, 1
+    bf = torch.bfloat16
+    wg, wu, wd = synth.mlp_weights(d, I, 0, cuda_device, bf)
+    x = synth.hidden(S, d, cuda_device, bf)
+    ref = torch.empty_like(x)
+    _mom.mlp_minseq_fwd(x, x, wg, wu, wd, ref, C)
+    sentinel = torch.full((world * S, d), -3.0, dtype=bf, device=cuda_device)
+    mine = sentinel.clone()
+    peers = [sentinel.clone() for _ in range(world - 1)]
+    sl = slice(rank * S, (rank + 1) * S)
+    x_host = x.cpu().pin_memory()
+    x_dev = torch.zeros_like(x)
+    free = torch.cuda.Event()
+    compute, cp = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(compute):
+        free.record(compute)
+        _mom.mlp_minseq_fwd_from_host_gather(x_host, x_dev, x_dev, wg, wu, wd, mine[sl], [p[sl] for p in peers], C,
+                                             stream=compute, copy_stream=cp, x_free=free)
+    torch.cuda.synchronize()
+    assert torch.equal(x_dev, x)
+    for buf in [mine] + peers:
+        assert torch.equal(buf[sl], ref)
+        assert torch.equal(buf[:rank * S], sentinel[:rank * S]) and torch.equal(buf[(rank + 1) * S:],
+                                                                                  sentinel[(rank + 1) * S:])
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
