@@ -43,6 +43,7 @@ SIGNATURES = {
     "mom_nccl_comm_destroy": (_i32, [_p]),
     "mom_allgather_rows": (_i32, [_p, _i64, _i64, _i32, _p, _i32, _i32, _p]),
     "mom_set_timing_events": (_i32, [_p, _p, _i64, _p]),
+    "mom_set_kernel_trace": (_i32, [_p, _i64, ctypes.POINTER(ctypes.c_int64)]),
     "mom_nccl_barrier": (_i32, [_p, _p, _p]),
     "mom_mlp_minseq_fwd_gather": (_i32, [_p, _p, _p, _p, _p, _p, _p, _i32, _i64, _i64, _i64, _i64, _i32, _p, _sz,
                                          _p]),

@@ -108,6 +108,18 @@ struct TimingHook {
 };
 thread_local TimingHook g_hook;
 
+// ---- per-thread in-kernel trace (mom_set_kernel_trace) ----
+struct TraceHook {
+  unsigned long long *buf = nullptr;
+  int64_t cap = 0;
+  int64_t *count = nullptr;
+};
+thread_local TraceHook g_trace;
+unsigned long long *next_trace_slot() {
+  if (!g_trace.buf || !g_trace.count || *g_trace.count >= g_trace.cap) return nullptr;
+  return g_trace.buf + (*g_trace.count)++ * (mom::kMaxTraceCtas * 4);
+}
+
 struct ScopedTiming {
   cudaStream_t s;
   int64_t slot = -1;
@@ -190,6 +202,19 @@ mom_status_t mom_set_timing_events(mom_event_t *events, int32_t *kinds, int64_t 
   g_hook.kinds = kinds;
   g_hook.cap = capacity;
   g_hook.count = count;
+  return MOM_OK;
+}
+
+mom_status_t mom_set_kernel_trace(void *dev_buf, int64_t capacity, int64_t *count) {
+  g_err[0] = 0;
+  if (!dev_buf) {
+    g_trace = TraceHook{};
+    return MOM_OK;
+  }
+  if (!count || capacity < 1 || !aligned16(dev_buf)) return fail(MOM_ERR_INVALID_ARG, "mom_set_kernel_trace: bad arguments");
+  g_trace.buf = static_cast<unsigned long long *>(dev_buf);
+  g_trace.cap = capacity;
+  g_trace.count = count;
   return MOM_OK;
 }
 
@@ -375,6 +400,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
       if (e != cudaSuccess) return cuda_fail(e, "counter reset");
       a.group_m = group_a;
       ScopedTiming tm(stream, 6);
+      a.trace = next_trace_slot();
       e = mom::launch_mlp_tc(a, 2, stream);
       if (e != cudaSuccess) return cuda_fail(e, "fused MLP (tcgen05)");
       continue;
@@ -386,6 +412,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     a.pdl = mlp_pdl && i > 0 && !x_host;
     {
       ScopedTiming tm(stream, 0);
+      a.trace = next_trace_slot();
       e = mom::launch_mlp_tc(a, 0, stream);  // H_i = Swish(A_i Wg^T) (.) A_i Wu^T
     }
     if (e != cudaSuccess) return cuda_fail(e, "phase A (tcgen05)");
@@ -395,6 +422,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     a.pdl = mlp_pdl;
     {
       ScopedTiming tm(stream, 1);
+      a.trace = next_trace_slot();
       e = mom::launch_mlp_tc(a, 1, stream);  // O_i = R_i + H_i Wd^T, written at rows r0..
     }
     if (e != cudaSuccess) return cuda_fail(e, "phase B (tcgen05)");

@@ -100,6 +100,7 @@ struct Params {
   uint32_t *ready;               // MODE_FUSED: per (row block, CTA rank) count of finished phase-A tiles
   uint32_t coalesced_a;          // phase-A epilogue through the smem stage (128-B row segments)
   uint32_t fast_silu;            // phase-A epilogue: quotient of the SiLU by rcp.approx (no branch)
+  unsigned long long *trace;     // instrumentation (mom_set_kernel_trace): per CTA 4 %globaltimer stamps, or null
   uint32_t n_peers;              // f1: extra destinations of the phase-B output rows
   __nv_bfloat16 *peer_out[kMaxPeers];  // f1: peers' gathered buffers, offset like `out`
   // f1 forwarding (warps 2-3): rows [0, fwd_rows) of fwd_src (the previous mini-sequence's
@@ -116,6 +117,11 @@ struct Tile {
   uint32_t hw;  // phase A: H columns of the tile (BHALF, or BHALF / 2 for a tail half tile)
 };
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -399,6 +405,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * C::STAGES + 4);
   uint8_t *epi_stage = smem + C::STAGES * C::STAGE_BYTES + 256;  // phase-B epilogue staging, 4 x 4 KB
 
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 4 + 0] = globaltimer_ns();  // entry
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
   const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0;
@@ -530,6 +537,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
+          if (p.trace && kb == 0 && t == cluster_id) p.trace[blockIdx.x * 4 + 1] = globaltimer_ns();  // first MMA
           const uint64_t adesc = ptx::sw128_kmajor_desc(ptx::smem_u32(smem_a + stage * A_BYTES));
           const uint64_t bdesc = ptx::sw128_kmajor_desc(ptx::smem_u32(smem_b + stage * C::B_BYTES));
 #pragma unroll
@@ -543,6 +551,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mma_commit<CG>(&tfull[acc], 0x3);      // accumulator ready for the epilogue(s)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
+      if (p.trace) p.trace[blockIdx.x * 4 + 2] = globaltimer_ns();  // last MMA issued
     }
   } else if (warp >= EPI_WARP0) {
     // ======================= epilogue: TMEM -> registers -> global =======================
@@ -620,6 +629,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<CG>(tmem_base, 2 * ACC_COLS);
   }
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 4 + 3] = globaltimer_ns();  // exit
 }
 
 template <int CG, int MODE>
@@ -700,6 +710,7 @@ static cudaError_t launch_mode(const TcMlpArgs &a, cudaStream_t stream) {
   p.ready = a.ready;
   p.coalesced_a = a.coalesced_a;
   p.fast_silu = a.fast_silu;
+  p.trace = a.trace;
   p.fwd_src = a.fwd_src;
   p.fwd_rows = a.fwd_rows;
   p.n_fwd = a.fwd_src ? a.n_fwd : 0;
