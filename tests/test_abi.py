@@ -138,6 +138,9 @@ def test_new_entry_points_reject_bad_arguments(lib):
     assert lib.mom_ipc_close(None, 0) == E
     assert lib.mom_set_timing_events(16, None, 4, None) == E
     assert lib.mom_set_timing_events(None, None, 0, None) == _mom.MOM_OK  # disabling is always fine
+    assert lib.mom_set_kernel_trace(16, 0, None) == E
+    assert lib.mom_set_kernel_trace(24, 4, ctypes.byref(ctypes.c_int64(0))) == E  # misaligned
+    assert lib.mom_set_kernel_trace(None, 0, None) == _mom.MOM_OK
     # rmsnorm workspace = plain workspace + C fp32 scales (rounded)
     base = lib.mom_mlp_minseq_workspace_bytes(4096, 512, 1024, 512, _mom.MOM_BF16)
     assert lib.mom_mlp_minseq_rmsnorm_workspace_bytes(4096, 512, 1024, 512, _mom.MOM_BF16) == base + 512 * 4
