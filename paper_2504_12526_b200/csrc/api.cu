@@ -117,7 +117,7 @@ struct TraceHook {
 thread_local TraceHook g_trace;
 unsigned long long *next_trace_slot() {
   if (!g_trace.buf || !g_trace.count || *g_trace.count >= g_trace.cap) return nullptr;
-  return g_trace.buf + (*g_trace.count)++ * (mom::kMaxTraceCtas * 4);
+  return g_trace.buf + (*g_trace.count)++ * (mom::kMaxTraceCtas * 8);
 }
 
 struct ScopedTiming {

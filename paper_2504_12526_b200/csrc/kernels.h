@@ -8,7 +8,7 @@
 
 namespace mom {
 
-constexpr uint32_t kMaxTraceCtas = 160;  // mom_set_kernel_trace: stamps per launch = 4 per CTA
+constexpr uint32_t kMaxTraceCtas = 160;  // mom_set_kernel_trace: 8 stamps per CTA per launch
 constexpr uint32_t kMaxPeers = 7;  // f1: up to 8 GPUs (7 peers) receive every phase-B output row
 
 // One mini-sequence on the tcgen05 path (mlp_tc.cu).  Tensor maps are 2D bf16, box 64 x 128.
@@ -29,7 +29,7 @@ struct TcMlpArgs {
   uint32_t *ready;           // fused mode: mlp_tc_ready_counters(rows) zeroed counters
   uint32_t coalesced_a;      // phase-A epilogue via the smem stage (coalesced H stores)
   uint32_t fast_silu;        // phase-A epilogue SiLU quotient by rcp.approx (MOM_FAST_SILU, default 1)
-  unsigned long long *trace; // instrumentation: kMaxTraceCtas x 4 %globaltimer stamps for this launch, or null
+  unsigned long long *trace; // instrumentation: kMaxTraceCtas x 8 stamps for this launch, or null
   uint32_t n_peers;          // f1: number of peer destinations (<= kMaxPeers)
   __nv_bfloat16 *peer_out[kMaxPeers];  // f1: peer gathered buffers at this mini-sequence's rows
   const __nv_bfloat16 *fwd_src;        // f1: previous mini-sequence's output rows to forward (or null)

@@ -100,7 +100,7 @@ struct Params {
   uint32_t *ready;               // MODE_FUSED: per (row block, CTA rank) count of finished phase-A tiles
   uint32_t coalesced_a;          // phase-A epilogue through the smem stage (128-B row segments)
   uint32_t fast_silu;            // phase-A epilogue: quotient of the SiLU by rcp.approx (no branch)
-  unsigned long long *trace;     // instrumentation (mom_set_kernel_trace): per CTA 4 %globaltimer stamps, or null
+  unsigned long long *trace;     // instrumentation (mom_set_kernel_trace): 8 stamps per CTA, or null
   uint32_t n_peers;              // f1: extra destinations of the phase-B output rows
   __nv_bfloat16 *peer_out[kMaxPeers];  // f1: peers' gathered buffers, offset like `out`
   // f1 forwarding (warps 2-3): rows [0, fwd_rows) of fwd_src (the previous mini-sequence's
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * C::STAGES + 4);
   uint8_t *epi_stage = smem + C::STAGES * C::STAGE_BYTES + 256;  // phase-B epilogue staging, 4 x 4 KB
 
-  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 4 + 0] = globaltimer_ns();  // entry
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 8 + 0] = globaltimer_ns();  // entry
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
   const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0;
@@ -537,7 +537,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          if (p.trace && kb == 0 && t == cluster_id) p.trace[blockIdx.x * 4 + 1] = globaltimer_ns();  // first MMA
+          if (p.trace && kb == 0 && t == cluster_id) {  // first MMA: time and SM cycle counter
+            p.trace[blockIdx.x * 8 + 1] = globaltimer_ns();
+            p.trace[blockIdx.x * 8 + 4] = clock64();
+          }
           const uint64_t adesc = ptx::sw128_kmajor_desc(ptx::smem_u32(smem_a + stage * A_BYTES));
           const uint64_t bdesc = ptx::sw128_kmajor_desc(ptx::smem_u32(smem_b + stage * C::B_BYTES));
 #pragma unroll
@@ -551,7 +554,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mma_commit<CG>(&tfull[acc], 0x3);      // accumulator ready for the epilogue(s)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
-      if (p.trace) p.trace[blockIdx.x * 4 + 2] = globaltimer_ns();  // last MMA issued
+      if (p.trace) {  // last MMA issued
+        p.trace[blockIdx.x * 8 + 2] = globaltimer_ns();
+        p.trace[blockIdx.x * 8 + 5] = clock64();
+      }
     }
   } else if (warp >= EPI_WARP0) {
     // ======================= epilogue: TMEM -> registers -> global =======================
@@ -629,7 +635,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<CG>(tmem_base, 2 * ACC_COLS);
   }
-  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 4 + 3] = globaltimer_ns();  // exit
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 8 + 3] = globaltimer_ns();  // exit
 }
 
 template <int CG, int MODE>

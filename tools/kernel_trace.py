@@ -19,7 +19,7 @@ with torch.cuda.stream(compute):
 torch.cuda.synchronize()
 steps = int(os.environ.get("STEPS", "3"))
 cap = steps * 2 * wl.M + 4
-buf = torch.zeros(cap * 160 * 4, dtype=torch.int64, device=dev)
+buf = torch.zeros(cap * 160 * 8, dtype=torch.int64, device=dev)
 count = ctypes.c_int64(0)
 _mom._check(_mom.lib().mom_set_kernel_trace(ctypes.c_void_p(buf.data_ptr()), cap, ctypes.byref(count)))
 with torch.cuda.stream(compute):
@@ -29,16 +29,18 @@ with torch.cuda.stream(compute):
 torch.cuda.synchronize()
 _mom.lib().mom_set_kernel_trace(None, 0, None)
 n = count.value
-t = buf.view(cap, 160, 4)[:n].cpu().numpy().astype("int64")
+t = buf.view(cap, 160, 8)[:n].cpu().numpy().astype("int64")
 rows = []
 for j in range(n):
-    ent, fm, lm, ex = (t[j, :, k] for k in range(4))
+    ent, fm, lm, ex, c0, c1 = (t[j, :, k] for k in range(6))
     used = ent > 0
     lead = fm > 0
+    mhz = statistics.median(((c1[lead] - c0[lead]) / (lm[lead] - fm[lead]) * 1e3).tolist())
     rows.append({"launch": j, "phase": "A" if j % 2 == 0 else "B", "ctas": int(used.sum()),
                  "entry_min": int(ent[used].min()), "entry_max": int(ent[used].max()),
                  "first_mma_min": int(fm[lead].min()), "first_mma_max": int(fm[lead].max()),
-                 "last_mma_min": int(lm[lead].min()), "last_mma_max": int(lm[lead].max()), "exit_max": int(ex[used].max())})
+                 "last_mma_min": int(lm[lead].min()), "last_mma_max": int(lm[lead].max()), "exit_max": int(ex[used].max()),
+                 "mhz": mhz})
 t0 = rows[0]["entry_min"]
 gaps = []
 for j, r in enumerate(rows):
@@ -48,10 +50,13 @@ for j, r in enumerate(rows):
     print(f'{j:3d} {r["phase"]} entry {(r["entry_min"]-t0)/1e3:9.1f}..{(r["entry_max"]-t0)/1e3:9.1f} '
           f'firstMMA {(r["first_mma_min"]-t0)/1e3:9.1f}..{(r["first_mma_max"]-t0)/1e3:9.1f} '
           f'lastMMA {(r["last_mma_min"]-t0)/1e3:9.1f}..{(r["last_mma_max"]-t0)/1e3:9.1f} exit {(r["exit_max"]-t0)/1e3:9.1f} us'
-          + ("" if g is None else f'  gap {g:7.1f}'))
+          + f' {r["mhz"]:6.0f} MHz' + ("" if g is None else f'  gap {g:7.1f}'))
 ga = [g for p, g in gaps if p == "B"]   # A(i) -> B(i)
 gb = [g for p, g in gaps if p == "A"]   # B(i) -> A(i+1)
 per_step_us = (rows[-1]["exit_max"] - rows[0]["entry_min"]) / 1e3 / steps
+mA = [r["mhz"] for r in rows if r["phase"] == "A"]
+mB = [r["mhz"] for r in rows if r["phase"] == "B"]
+print(json.dumps({"phaseA_mhz_median": round(statistics.median(mA)), "phaseB_mhz_median": round(statistics.median(mB))}))
 print(json.dumps({"launches": n, "A_to_B_gap_us_mean": round(statistics.mean(ga), 2),
                   "B_to_A_gap_us_mean": round(statistics.mean(gb), 2) if gb else None,
                   "mlp_wall_us_per_step": round(per_step_us, 1),
