@@ -139,10 +139,15 @@ def _dt(t: torch.Tensor) -> int:
 
 
 def _ptr(t):
+    """Raw pointer of a tensor argument.  The C ABI takes dense row-major buffers: a strided view
+    (e.g. a transposed weight) would be read with the wrong layout, so it is rejected here."""
     if t is None:
         return None
     if isinstance(t, int):
         return t
+    if not t.is_contiguous():
+        raise ValueError(f"libmom takes contiguous row-major tensors (got shape {tuple(t.shape)}, "
+                         f"stride {tuple(t.stride())})")
     return t.data_ptr()
 
 

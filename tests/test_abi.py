@@ -144,3 +144,15 @@ def test_new_entry_points_reject_bad_arguments(lib):
     # rmsnorm workspace = plain workspace + C fp32 scales (rounded)
     base = lib.mom_mlp_minseq_workspace_bytes(4096, 512, 1024, 512, _mom.MOM_BF16)
     assert lib.mom_mlp_minseq_rmsnorm_workspace_bytes(4096, 512, 1024, 512, _mom.MOM_BF16) == base + 512 * 4
+
+
+def test_binding_rejects_strided_views():
+    """A transposed / strided tensor would be read as row-major by the kernels: the binding refuses it."""
+    import torch
+    w = torch.zeros(16, 8)
+    assert _mom._ptr(w) == w.data_ptr()
+    assert _mom._ptr(w[3]) == w[3].data_ptr()       # a row view is dense
+    with pytest.raises(ValueError):
+        _mom._ptr(w.t())
+    with pytest.raises(ValueError):
+        _mom._ptr(w[:, :4])
