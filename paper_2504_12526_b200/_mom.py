@@ -185,8 +185,34 @@ def mlp_minseq_workspace_bytes(S: int, hidden: int, intermediate: int, minseq_le
     return int(lib().mom_mlp_minseq_workspace_bytes(S, hidden, intermediate, minseq_len, dt))
 
 
+def _expect(name, t, shape, dtype):
+    if t is None:
+        return
+    if tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+        raise ValueError(f"{name}: expected shape {tuple(shape)} dtype {dtype}, got {tuple(t.shape)} {t.dtype}")
+
+
+def _check_mlp(x, residual, w_gate, w_up, w_down, out, x_host=None):
+    """Shapes of the MLP arguments (the C ABI trusts the sizes it is given): x, residual, out, x_host
+    [S, d]; W_gate, W_up [I, d]; W_down [d, I]; one dtype."""
+    if x.dim() != 2 or w_gate.dim() != 2:
+        raise ValueError("x and w_gate must be 2-D")
+    (S, d), I = x.shape, w_gate.shape[0]
+    for name, t, shape in (("residual", residual, (S, d)), ("w_gate", w_gate, (I, d)), ("w_up", w_up, (I, d)),
+                           ("w_down", w_down, (d, I)), ("out", out, (S, d)), ("x_host", x_host, (S, d))):
+        _expect(name, t, shape, x.dtype)
+
+
+def _check_gemv(x, residual, w_gate, w_up, w_down, out):
+    d, I = x.shape[-1], w_gate.shape[0]
+    for name, t, shape in (("x_last", x, (d,)), ("residual_last", residual, (d,)), ("w_gate", w_gate, (I, d)),
+                           ("w_up", w_up, (I, d)), ("w_down", w_down, (d, I)), ("out_last", out, (d,))):
+        _expect(name, t, shape, x.dtype)
+
+
 def mlp_minseq_fwd(x, residual, w_gate, w_up, w_down, out, minseq_len: int, workspace=None, stream=None):
     """Alg. 1: out = residual + concat_i MLP(x_i) over M = ceil(S/C) mini-sequences."""
+    _check_mlp(x, residual, w_gate, w_up, w_down, out)
     S, hidden = x.shape
     I = w_gate.shape[0]
     dt = _dt(x)
@@ -204,6 +230,7 @@ def mlp_minseq_fwd_from_host(x_host, x, residual, w_gate, w_up, w_down, out, min
     """End-to-end entry: x_host (pinned) is streamed into x one mini-sequence at a time on
     copy_stream while the MLP of the previous mini-sequence runs on stream.  x_free: optional
     torch.cuda.Event after which x is free (the copies wait on it instead of on `stream`)."""
+    _check_mlp(x, residual, w_gate, w_up, w_down, out, x_host)
     S, hidden = x.shape
     I = w_gate.shape[0]
     dt = _dt(x)
@@ -245,6 +272,7 @@ def mlp_minseq_rmsnorm_fwd(x, w_gate_folded, w_up_folded, w_down, out, minseq_le
 
 def mlp_last_token(x_last, residual_last, w_gate, w_up, w_down, out_last, workspace=None, stream=None):
     """Alg. 1: O_last = residual_last + MLP(A_last) on one token (GEMV pair)."""
+    _check_gemv(x_last, residual_last, w_gate, w_up, w_down, out_last)
     hidden = x_last.shape[-1]
     I = w_gate.shape[0]
     dt = _dt(x_last)
@@ -260,6 +288,11 @@ def lm_head_last(h_last, norm_gain, eps: float, w_head, logits, argmax, workspac
     """Alg. 1: logits = W_head . rmsnorm(h_last) (fp32) and argmax (int32, ties -> lowest)."""
     hidden = h_last.shape[-1]
     V = w_head.shape[0]
+    _expect("h_last", h_last, (hidden,), h_last.dtype)
+    _expect("norm_gain", norm_gain, (hidden,), h_last.dtype)
+    _expect("w_head", w_head, (V, hidden), h_last.dtype)
+    _expect("logits", logits, (V,), torch.float32)
+    _expect("argmax", argmax, (1,), torch.int32)
     dt = _dt(h_last)
     if workspace is None:
         workspace = torch.empty(lib().mom_lm_head_workspace_bytes(V), dtype=torch.uint8, device=h_last.device)
@@ -313,6 +346,7 @@ def mlp_minseq_fwd_gather(x, residual, w_gate, w_up, w_down, out, peer_out, mins
                           stream=None):
     """f1: mlp_minseq_fwd whose phase-B epilogue also stores every output row into each peer
     buffer (device pointers, e.g. from ipc_open_handle, offset like `out`)."""
+    _check_mlp(x, residual, w_gate, w_up, w_down, out)
     S, hidden = x.shape
     I = w_gate.shape[0]
     dt = _dt(x)
@@ -331,6 +365,7 @@ def mlp_minseq_fwd_from_host_gather(x_host, x, residual, w_gate, w_up, w_down, o
                                     workspace=None, stream=None, copy_stream=None, x_free=None):
     """End-to-end entry of token-sharded runs: mlp_minseq_fwd_from_host whose output rows also go
     to every peer buffer (as mlp_minseq_fwd_gather)."""
+    _check_mlp(x, residual, w_gate, w_up, w_down, out, x_host)
     S, hidden = x.shape
     I = w_gate.shape[0]
     dt = _dt(x)

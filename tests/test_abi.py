@@ -156,3 +156,22 @@ def test_binding_rejects_strided_views():
         _mom._ptr(w.t())
     with pytest.raises(ValueError):
         _mom._ptr(w[:, :4])
+
+
+def test_binding_checks_shapes():
+    """The C ABI trusts the sizes it is given: the binding refuses inconsistent tensors before any call."""
+    import torch
+    bf = torch.bfloat16
+    S, d, I = 8, 16, 24
+    x, out = torch.zeros(S, d, dtype=bf), torch.zeros(S, d, dtype=bf)
+    wg, wu, wd = torch.zeros(I, d, dtype=bf), torch.zeros(I, d, dtype=bf), torch.zeros(d, I, dtype=bf)
+    with pytest.raises(ValueError):
+        _mom.mlp_minseq_fwd(x, x, wg, wu, wd.t().contiguous(), out, 4)       # W_down as [I, d]
+    with pytest.raises(ValueError):
+        _mom.mlp_minseq_fwd(x, x, wg, torch.zeros(I + 8, d, dtype=bf), wd, out, 4)
+    with pytest.raises(ValueError):
+        _mom.mlp_minseq_fwd(x, x, wg, wu, wd, torch.zeros(S, d), 4)          # fp32 out for bf16 x
+    with pytest.raises(ValueError):
+        _mom.mlp_last_token(x[0], x[0], wg, wu, wd, torch.zeros(d + 8, dtype=bf))
+    with pytest.raises(ValueError):
+        _mom.lm_head_last(x[0], None, 1e-5, torch.zeros(40, d, dtype=bf), torch.zeros(41), torch.zeros(1, dtype=torch.int32))
