@@ -83,3 +83,61 @@ def test_shard_plan_edges():
     assert last_token_owner(9, 4) == 2  # per = 3: rows 6..8 on rank 2, rank 3 holds only padding
     with pytest.raises(ValueError):
         shard_rows(10, 0, 0)
+
+
+# ---------------------------------------------------------------- f2: vocab-sharded LM head protocol
+def _pack_key(v: np.float32, idx: int) -> int:
+    """The kernels' argmax key (gemv.cu pack_key, include/mom.h f2): order-preserving float -> u32 in
+    the high word, complemented GLOBAL vocab index in the low word, so the u64 max is the largest
+    logit and, among equal logits, the lowest index."""
+    b = int(np.float32(v).view(np.uint32))
+    b = (~b & 0xFFFFFFFF) if (b & 0x80000000) else (b | 0x80000000)
+    return (b << 32) | (0xFFFFFFFF - idx)
+
+
+def _head_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        V, d = 1000, 32
+        r = np.random.default_rng(9)
+        h = r.standard_normal(d).astype(np.float32)
+        w = (r.standard_normal((V, d)) * 0.1).astype(np.float32)
+        w[700] = w[10] = w[int(np.argmax(w @ h))] * 1.0 + 0.5 * h / np.linalg.norm(h)  # a tie across shards
+        per = V // world
+        lo = rank * per
+        logits = oracle.lm_head(h.astype(np.float64), w[lo:lo + per])[0].astype(np.float32)  # fp32 like the kernel
+        best = max(_pack_key(v, lo + i) for i, v in enumerate(logits))
+        # gloo has no uint64 max: flip the top bit so signed int64 order equals u64 order
+        t = torch.tensor([best ^ (1 << 63)], dtype=torch.uint64).view(torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        key = int(t.view(torch.uint64).item()) ^ (1 << 63)
+        q.put((rank, 0xFFFFFFFF - (key & 0xFFFFFFFF)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_vocab_sharded_argmax_protocol():
+    """f2: each rank reduces its vocab shard to one packed key, one u64 max across the
+    ranks gives the global argmax -- ties across shards resolve to the lowest index."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_head_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert {idx for _, idx in res} == {10}  # rows 10 (rank 0) and 700 (rank 1) tie at the max
+
+
+def test_pack_key_orders_like_floats():
+    vals = np.array([-np.inf, -3.5, -1e-30, -0.0, 0.0, 1e-30, 2.0, 2.0, np.inf], np.float32)
+    keys = [_pack_key(v, i) for i, v in enumerate(vals)]
+    assert keys[7] < keys[6]                     # equal values: the lower index has the larger key
+    order = sorted(range(len(vals)), key=lambda i: keys[i])
+    assert [float(vals[i]) for i in order] == sorted(float(v) for v in vals)
