@@ -52,3 +52,41 @@ def test_transient_memory_is_one_minisequence(cuda_device):
     assert S * I * 2 <= peaks[S] <= S * I * 2 + (1 << 20)
     ratio = peaks[S] / peaks[C]
     assert M * 0.99 <= ratio <= M * 1.01
+
+
+def test_concurrent_calls_from_two_threads(cuda_device):
+    """include/mom.h claims thread safety: two host threads issuing calls on their own streams (own
+    workspaces) at the same time get exactly the single-threaded results."""
+    import threading
+    S, d, I, C = 1200, 512, 1024, 300
+    bf = torch.bfloat16
+    wg, wu, wd = synth.mlp_weights(d, I, 0, cuda_device, bf)
+    xs = [synth.hidden(S, d, cuda_device, bf, seed=synth.SEED_X + k) for k in range(2)]
+    refs = []
+    for x in xs:
+        o = torch.empty_like(x)
+        _mom.mlp_minseq_fwd(x, x, wg, wu, wd, o, C)
+        refs.append(o)
+    torch.cuda.synchronize()
+    outs = [torch.empty_like(x) for x in xs]
+    errors = []
+
+    def work(k):
+        try:
+            s = torch.cuda.Stream(cuda_device)
+            with torch.cuda.stream(s):
+                for _ in range(5):
+                    _mom.mlp_minseq_fwd(xs[k], xs[k], wg, wu, wd, outs[k], C, stream=s)
+            s.synchronize()
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errors, errors
+    for k in range(2):
+        assert torch.equal(outs[k], refs[k])
