@@ -63,3 +63,36 @@ def test_pipelined_steps_equal_one_request(cuda_device, e2e, serial):
     assert torch.equal(wl.kv_back, wl.kv)
     for slot in wl.kv_host:
         assert torch.equal(slot, wl.kv.cpu())
+
+
+def test_bench_step_full_size_vs_oracle(cuda_device):
+    """BASELINE config 2 at full size in exactly the bench's launch configuration (pipelined requests,
+    PDL, KV copies in flight, then the e2e leg with host input): sampled output rows against the
+    oracle, the last token's MLP against the oracle, and the argmax against the oracle's logits of
+    the kernel's own hidden vector."""
+    import oracle
+    from tests.parity import TOL_BF16, argmax_matches, check_close
+    cfg = synth.CONFIGS[1]
+    wl = bench.Workload(cfg, 0, 1, cuda_device)
+    compute, copy, reload = (torch.cuda.Stream(cuda_device) for _ in range(3))
+    h2d = torch.cuda.Stream(cuda_device)
+    x_host = wl.x.cpu().pin_memory()
+    wl.init_e2e(compute)
+    with torch.cuda.stream(compute):
+        for _ in range(2):
+            bench.run_step(wl, compute, copy, reload, [0])
+        for _ in range(2):
+            bench.run_step(wl, compute, copy, reload, [0], x_host=x_host, h2d=h2d)
+        bench.flush_reload(wl, h2d)
+        bench.join_streams(compute, copy, reload, h2d)
+    torch.cuda.synchronize()
+    rows = synth.sample_rows(wl.S, wl.C, n_random=32)
+    xs = wl.x.cpu()
+    wg, wu, wd = (t.cpu() for t in wl.w0)
+    check_close(wl.out[rows].cpu(), oracle.mlp_rows(xs, xs, wg, wu, wd, rows), TOL_BF16, "bench step rows")
+    last = wl.out[-1].cpu()
+    wg1, wu1, wd1 = (t.cpu() for t in wl.w1)
+    check_close(wl.y.cpu(), oracle.mlp_rows(last[None], last[None], wg1, wu1, wd1, [0])[0], TOL_BF16, "last token")
+    yn = oracle.rmsnorm(wl.y.cpu().double().numpy(), wl.gain.cpu(), cfg.eps)
+    ref_logits = oracle.lm_head(yn, wl.wh.cpu())[0]
+    assert argmax_matches(int(wl.argmax.item()), ref_logits) in ("exact", "near-tie")
