@@ -291,7 +291,8 @@ mom_status_t mom_set_timing_events(mom_event_t *events, int32_t *kinds, int64_t 
  * thread, the j-th tcgen05 MLP launch (j = *count before it, j < capacity) writes stamps to
  * dev_buf[(j * 160 + cta) * 8 + k]: %globaltimer (ns) at k = 0 CTA entry, 1 first MMA issued and
  * 2 last MMA issued (leader CTAs), 3 CTA exit; the SM's clock64 at k = 4 first and 5 last MMA
- * (so the SM clock over the launch is (k5 - k4) / (k2 - k1)); *count is incremented per launch.
+ * (so the SM clock over the launch is (k5 - k4) / (k2 - k1)); k = 6 the SM cycles epilogue warp 4
+ * spent in tile epilogues (summed), k = 7 their count; *count is incremented per launch.
  * dev_buf: device uint64[capacity * 160 * 8], zeroed by the caller.  NULL disables. */
 mom_status_t mom_set_kernel_trace(void *dev_buf, int64_t capacity, int64_t *count);
 

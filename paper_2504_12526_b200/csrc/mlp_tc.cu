@@ -575,6 +575,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t row = tl.m * BM * CG + rank * BM + row_in_tile;
       const bool row_ok = row < p.rows;
       const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * ACC_COLS;
+      const unsigned long long epi_t0 = p.trace ? clock64() : 0ull;
       if (tl.a && p.coalesced_a && p.fast_silu)
         epilogue_a_coalesced<true>(p, taddr, row - lane, tl.c0, tl.hw, epi_stage + q * 32 * 128);
       else if (tl.a && p.coalesced_a)
@@ -585,6 +586,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         epilogue_a<false>(p, taddr, row, row_ok, tl.c0, tl.hw);
       else
         epilogue_b(p, taddr, row - lane, tl.n * p.nb, epi_stage + q * 32 * 128);
+      if (p.trace && q == 0 && lane == 0) {  // epilogue cycles of warp 4 (summed) and tile count
+        p.trace[blockIdx.x * 8 + 6] += clock64() - epi_t0;
+        p.trace[blockIdx.x * 8 + 7] += 1;
+      }
       // release the accumulator to the MMA issuer
       ptx::tc_fence_before();
       __syncwarp();

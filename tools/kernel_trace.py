@@ -36,11 +36,13 @@ for j in range(n):
     used = ent > 0
     lead = fm > 0
     mhz = statistics.median(((c1[lead] - c0[lead]) / (lm[lead] - fm[lead]) * 1e3).tolist())
+    ecyc, ecnt = t[j, :, 6], t[j, :, 7]
+    epi = float(ecyc[used].sum() / max(1, ecnt[used].sum()))  # mean epilogue cycles per tile (warp 4)
     rows.append({"launch": j, "phase": "A" if j % 2 == 0 else "B", "ctas": int(used.sum()),
                  "entry_min": int(ent[used].min()), "entry_max": int(ent[used].max()),
                  "first_mma_min": int(fm[lead].min()), "first_mma_max": int(fm[lead].max()),
                  "last_mma_min": int(lm[lead].min()), "last_mma_max": int(lm[lead].max()), "exit_max": int(ex[used].max()),
-                 "mhz": mhz})
+                 "mhz": mhz, "epi_cycles": epi})
 t0 = rows[0]["entry_min"]
 gaps = []
 for j, r in enumerate(rows):
@@ -50,13 +52,17 @@ for j, r in enumerate(rows):
     print(f'{j:3d} {r["phase"]} entry {(r["entry_min"]-t0)/1e3:9.1f}..{(r["entry_max"]-t0)/1e3:9.1f} '
           f'firstMMA {(r["first_mma_min"]-t0)/1e3:9.1f}..{(r["first_mma_max"]-t0)/1e3:9.1f} '
           f'lastMMA {(r["last_mma_min"]-t0)/1e3:9.1f}..{(r["last_mma_max"]-t0)/1e3:9.1f} exit {(r["exit_max"]-t0)/1e3:9.1f} us'
-          + f' {r["mhz"]:6.0f} MHz' + ("" if g is None else f'  gap {g:7.1f}'))
+          + f' {r["mhz"]:6.0f} MHz epi {r["epi_cycles"]:7.0f} cyc' + ("" if g is None else f'  gap {g:7.1f}'))
 ga = [g for p, g in gaps if p == "B"]   # A(i) -> B(i)
 gb = [g for p, g in gaps if p == "A"]   # B(i) -> A(i+1)
 per_step_us = (rows[-1]["exit_max"] - rows[0]["entry_min"]) / 1e3 / steps
 mA = [r["mhz"] for r in rows if r["phase"] == "A"]
 mB = [r["mhz"] for r in rows if r["phase"] == "B"]
-print(json.dumps({"phaseA_mhz_median": round(statistics.median(mA)), "phaseB_mhz_median": round(statistics.median(mB))}))
+eA = [r["epi_cycles"] for r in rows if r["phase"] == "A"]
+eB = [r["epi_cycles"] for r in rows if r["phase"] == "B"]
+print(json.dumps({"phaseA_mhz_median": round(statistics.median(mA)), "phaseB_mhz_median": round(statistics.median(mB)),
+                  "phaseA_epilogue_cycles_per_tile": round(statistics.median(eA)),
+                  "phaseB_epilogue_cycles_per_tile": round(statistics.median(eB))}))
 print(json.dumps({"launches": n, "A_to_B_gap_us_mean": round(statistics.mean(ga), 2),
                   "B_to_A_gap_us_mean": round(statistics.mean(gb), 2) if gb else None,
                   "mlp_wall_us_per_step": round(per_step_us, 1),
