@@ -333,6 +333,71 @@ def join_streams(compute, *others):
         compute.wait_stream(s)
 
 
+def kernel_trace_pass(wl, compute, copy, reload, steps: int = 2):
+    """In-kernel timeline of the tcgen05 launches of `steps` pipelined steps (mom_set_kernel_trace:
+    %globaltimer + clock64 per CTA, no host events, so PDL overlap is intact).  Per phase: the SM clock
+    over the launch and the MMA-issue efficiency -- the cycles from a launch's first to its last MMA
+    issue against the tcgen05 rate (one 256 x 256 x 16 pair MMA per 128 cycles, 8192 bf16 FLOP per SM
+    per cycle) for the busiest cluster's tiles."""
+    import ctypes
+    from paper_2504_12526_b200 import _mom
+    cap = steps * 2 * wl.M + 4
+    buf = torch.zeros(cap * 160 * 8, dtype=torch.int64, device=wl.device)
+    count = ctypes.c_int64(0)
+    _mom._check(_mom.lib().mom_set_kernel_trace(ctypes.c_void_p(buf.data_ptr()), cap, ctypes.byref(count)))
+    try:
+        with torch.cuda.stream(compute):
+            for _ in range(steps):
+                run_step(wl, compute, copy, reload, [0])
+            join_streams(compute, copy, reload)
+        torch.cuda.synchronize()
+    finally:
+        _mom.lib().mom_set_kernel_trace(None, 0, None)
+    t = buf.view(cap, 160, 8)[:count.value].cpu().numpy().astype("int64")
+    clusters = torch.cuda.get_device_properties(wl.device).multi_processor_count // 2
+    kbA, kbB = -(-wl.d // 64), -(-wl.I // 64)
+    nA, nb = -(-wl.I // 128), 256
+    res = {"A": {"mhz": [], "eff": []}, "B": {"mhz": [], "eff": []}, "gap_us": [], "step_eff": []}
+    step_ideal, step_first = 0.0, None
+    for j in range(t.shape[0]):
+        i = (j // 2) % wl.M                       # mini-sequence of this launch
+        rows = min(wl.C, wl.S - i * wl.C)
+        m_tiles = -(-rows // 256)
+        fm, lm, c0, c1 = t[j, :, 1], t[j, :, 2], t[j, :, 4], t[j, :, 5]
+        lead = fm > 0
+        mhz = statistics.median(((c1[lead] - c0[lead]) / (lm[lead] - fm[lead]) * 1e3).tolist())
+        span_cycles = (lm[lead].max() - fm[lead].min()) * mhz / 1e3
+        if j % 2 == 0:
+            T = m_tiles * nA
+            R = T % clusters
+            ideal = ((T - R) // clusters * kbA * 512 + kbA * 256) if 0 < 2 * R <= clusters else -(-T // clusters) * kbA * 512
+            ph = "A"
+        else:
+            # phase-B tile width 256 (the library picks another width only when d % 256 != 0)
+            T = m_tiles * -(-wl.d // nb)
+            ideal = -(-T // clusters) * kbB * 512 if wl.d % 256 == 0 else float("nan")
+            ph = "B"
+            res["gap_us"].append((fm[lead].min() - t[j - 1, :, 2][t[j - 1, :, 1] > 0].max()) / 1e3)
+        res[ph]["mhz"].append(mhz)
+        res[ph]["eff"].append(ideal / span_cycles)
+        # whole-step MLP: ideal cycles of all its launches over the span from the step's first MMA
+        # issue to its last (launch overlaps under PDL counted once)
+        if j % (2 * wl.M) == 0:
+            step_ideal, step_first = 0.0, fm[lead].min()
+        step_ideal += ideal
+        if j % (2 * wl.M) == 2 * wl.M - 1:
+            res["step_eff"].append(step_ideal / ((lm[lead].max() - step_first) * mhz / 1e3))
+    return {"phaseA_mhz": round(statistics.median(res["A"]["mhz"])), "phaseB_mhz": round(statistics.median(res["B"]["mhz"])),
+            "mlp_step_mma_issue_efficiency": round(statistics.median(res["step_eff"]), 4),
+            "phaseA_mma_issue_efficiency": round(statistics.median(res["A"]["eff"]), 4),
+            "phaseB_mma_issue_efficiency": round(statistics.median(res["B"]["eff"]), 4),
+            "note": "phase A's span includes its PDL-staggered start (its first CTAs run beside phase B's last "
+                    "wave), so the per-phase figures split the overlap unevenly; the step figure counts it once",
+            "A_to_B_gap_us": round(statistics.median(res["gap_us"]), 2), "launches": int(t.shape[0]),
+            "method": "mom_set_kernel_trace: %globaltimer/clock64 stamps per CTA; efficiency = ideal issue cycles "
+                      "(128 per 256x256x16 pair MMA, busiest cluster's tiles) / cycles from first to last MMA issue"}
+
+
 def measure_peak_activation(wl, C):
     """Peak extra device bytes of one mini-sequence MLP call (workspace allocated by the call)."""
     from paper_2504_12526_b200 import _mom
@@ -540,6 +605,11 @@ def run_mine(args):
         "gpu_launches": n_launch,
     }
     result["clocks"] = clk.summary()
+    if world == 1 and cfg.dtype == "bf16":
+        try:
+            result["kernel_trace"] = kernel_trace_pass(wl, compute, copy, reload)
+        except Exception as e:  # instrumentation only: never fails the bench line
+            result["kernel_trace"] = {"error": str(e)[:200]}
     result["ms_per_step_event_timed"] = ms_event_timed
     result["config"]["requests"] = ("serial: request i+1 waits for request i's KV reload" if args.serial else
                                     "pipelined: request i's KV reload (H2D) overlaps request i+1's MLP")
