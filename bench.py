@@ -333,35 +333,36 @@ def join_streams(compute, *others):
         compute.wait_stream(s)
 
 
-def kernel_trace_pass(wl, compute, copy, reload, steps: int = 2):
-    """In-kernel timeline of the tcgen05 launches of `steps` pipelined steps (mom_set_kernel_trace:
-    %globaltimer + clock64 per CTA, no host events, so PDL overlap is intact).  Per phase: the SM clock
-    over the launch and the MMA-issue efficiency -- the cycles from a launch's first to its last MMA
-    issue against the tcgen05 rate (one 256 x 256 x 16 pair MMA per 128 cycles, 8192 bf16 FLOP per SM
-    per cycle) for the busiest cluster's tiles."""
-    import ctypes
-    from paper_2504_12526_b200 import _mom
-    cap = steps * 2 * wl.M + 4
-    buf = torch.zeros(cap * 160 * 8, dtype=torch.int64, device=wl.device)
-    count = ctypes.c_int64(0)
-    _mom._check(_mom.lib().mom_set_kernel_trace(ctypes.c_void_p(buf.data_ptr()), cap, ctypes.byref(count)))
-    try:
-        with torch.cuda.stream(compute):
-            for _ in range(steps):
-                run_step(wl, compute, copy, reload, [0])
-            join_streams(compute, copy, reload)
-        torch.cuda.synchronize()
-    finally:
-        _mom.lib().mom_set_kernel_trace(None, 0, None)
-    t = buf.view(cap, 160, 8)[:count.value].cpu().numpy().astype("int64")
-    clusters = torch.cuda.get_device_properties(wl.device).multi_processor_count // 2
-    kbA, kbB = -(-wl.d // 64), -(-wl.I // 64)
-    nA, nb = -(-wl.I // 128), 256
-    res = {"A": {"mhz": [], "eff": []}, "B": {"mhz": [], "eff": []}, "gap_us": [], "step_eff": []}
-    step_ideal, step_first = 0.0, None
+def phase_b_width(m_tiles: int, d: int, clusters: int) -> int:
+    """The phase-B tile width the library picks (api.cu pick_phase_b_width: MOM_NB_B, else 256 unless
+    an exact divisor of d in 224..128 beats it by > 5 % in the wave-quantisation model)."""
+    forced = int(os.environ.get("MOM_NB_B", "0") or 0)
+    if 32 <= forced <= 256 and forced % 32 == 0:
+        return forced
+    cost = lambda nb: -(-(m_tiles * -(-d // nb)) // clusters) * nb
+    base, best, best_cost = cost(256), 256, cost(256)
+    for nb in range(224, 127, -32):
+        if d % nb == 0 and cost(nb) * 100 < base * 95 and cost(nb) < best_cost:
+            best, best_cost = nb, cost(nb)
+    return best
+
+
+def trace_efficiency(t, S: int, C: int, d: int, I: int, num_sms: int):
+    """Parse mom_set_kernel_trace stamps t [launches, 160, 8] of consecutive calls of one mini-sequence
+    MLP shape (launch order A(0), B(0), ..., A(M-1), B(M-1) per call).  Per phase: the SM clock over
+    the launch and the MMA-issue efficiency -- the cycles from a launch's first to its last MMA issue
+    against the tcgen05 rate (one 256 x 256 x 16 pair MMA per 128 cycles, 8192 bf16 FLOP per SM per
+    cycle) for the busiest cluster's tiles; per call: the same over the span from the call's first to
+    its last MMA issue (PDL overlaps counted once)."""
+    M = -(-S // C)
+    clusters = num_sms // 2
+    kbA, kbB = -(-d // 64), -(-I // 64)
+    nA = -(-I // 128)
+    res = {"A": {"mhz": [], "eff": []}, "B": {"mhz": [], "eff": []}, "gap_us": [], "call_eff": []}
+    call_ideal, call_first = 0.0, None
     for j in range(t.shape[0]):
-        i = (j // 2) % wl.M                       # mini-sequence of this launch
-        rows = min(wl.C, wl.S - i * wl.C)
+        i = (j // 2) % M                       # mini-sequence of this launch
+        rows = min(C, S - i * C)
         m_tiles = -(-rows // 256)
         fm, lm, c0, c1 = t[j, :, 1], t[j, :, 2], t[j, :, 4], t[j, :, 5]
         lead = fm > 0
@@ -373,29 +374,55 @@ def kernel_trace_pass(wl, compute, copy, reload, steps: int = 2):
             ideal = ((T - R) // clusters * kbA * 512 + kbA * 256) if 0 < 2 * R <= clusters else -(-T // clusters) * kbA * 512
             ph = "A"
         else:
-            # phase-B tile width 256 (the library picks another width only when d % 256 != 0)
-            T = m_tiles * -(-wl.d // nb)
-            ideal = -(-T // clusters) * kbB * 512 if wl.d % 256 == 0 else float("nan")
+            w_b = phase_b_width(m_tiles, d, clusters)
+            T = m_tiles * -(-d // w_b)
+            ideal = -(-T // clusters) * kbB * 512 * w_b / 256    # UMMA N = w_b: 128 * w_b / 256 cycles
             ph = "B"
             res["gap_us"].append((fm[lead].min() - t[j - 1, :, 2][t[j - 1, :, 1] > 0].max()) / 1e3)
         res[ph]["mhz"].append(mhz)
         res[ph]["eff"].append(ideal / span_cycles)
-        # whole-step MLP: ideal cycles of all its launches over the span from the step's first MMA
-        # issue to its last (launch overlaps under PDL counted once)
-        if j % (2 * wl.M) == 0:
-            step_ideal, step_first = 0.0, fm[lead].min()
-        step_ideal += ideal
-        if j % (2 * wl.M) == 2 * wl.M - 1:
-            res["step_eff"].append(step_ideal / ((lm[lead].max() - step_first) * mhz / 1e3))
+        if j % (2 * M) == 0:
+            call_ideal, call_first = 0.0, fm[lead].min()
+        call_ideal += ideal
+        if j % (2 * M) == 2 * M - 1:
+            res["call_eff"].append(call_ideal / ((lm[lead].max() - call_first) * mhz / 1e3))
+    med = lambda v: round(statistics.median(v), 4) if v else None
     return {"phaseA_mhz": round(statistics.median(res["A"]["mhz"])), "phaseB_mhz": round(statistics.median(res["B"]["mhz"])),
-            "mlp_step_mma_issue_efficiency": round(statistics.median(res["step_eff"]), 4),
-            "phaseA_mma_issue_efficiency": round(statistics.median(res["A"]["eff"]), 4),
-            "phaseB_mma_issue_efficiency": round(statistics.median(res["B"]["eff"]), 4),
+            "mlp_step_mma_issue_efficiency": med(res["call_eff"]),
+            "phaseA_mma_issue_efficiency": med(res["A"]["eff"]),
+            "phaseB_mma_issue_efficiency": med(res["B"]["eff"]),
             "note": "phase A's span includes its PDL-staggered start (its first CTAs run beside phase B's last "
                     "wave), so the per-phase figures split the overlap unevenly; the step figure counts it once",
             "A_to_B_gap_us": round(statistics.median(res["gap_us"]), 2), "launches": int(t.shape[0]),
             "method": "mom_set_kernel_trace: %globaltimer/clock64 stamps per CTA; efficiency = ideal issue cycles "
                       "(128 per 256x256x16 pair MMA, busiest cluster's tiles) / cycles from first to last MMA issue"}
+
+
+def kernel_traced(fn, capacity: int, device):
+    """Run fn() with mom_set_kernel_trace enabled; returns the stamps [launches, 160, 8] (int64 numpy)."""
+    import ctypes
+    from paper_2504_12526_b200 import _mom
+    buf = torch.zeros(capacity * 160 * 8, dtype=torch.int64, device=device)
+    count = ctypes.c_int64(0)
+    _mom._check(_mom.lib().mom_set_kernel_trace(ctypes.c_void_p(buf.data_ptr()), capacity, ctypes.byref(count)))
+    try:
+        fn()
+        torch.cuda.synchronize()
+    finally:
+        _mom.lib().mom_set_kernel_trace(None, 0, None)
+    return buf.view(capacity, 160, 8)[:count.value].cpu().numpy().astype("int64")
+
+
+def kernel_trace_pass(wl, compute, copy, reload, steps: int = 2):
+    """In-kernel timeline of the tcgen05 launches of `steps` pipelined steps (no host events, so PDL
+    overlap is intact): SM clock and MMA-issue efficiency (trace_efficiency)."""
+    def run():
+        with torch.cuda.stream(compute):
+            for _ in range(steps):
+                run_step(wl, compute, copy, reload, [0])
+            join_streams(compute, copy, reload)
+    t = kernel_traced(run, steps * 2 * wl.M + 4, wl.device)
+    return trace_efficiency(t, wl.S, wl.C, wl.d, wl.I, torch.cuda.get_device_properties(wl.device).multi_processor_count)
 
 
 def measure_peak_activation(wl, C):

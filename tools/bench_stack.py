@@ -21,7 +21,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import synth  # noqa: E402
-from bench import ClockSampler, load_peaks  # noqa: E402
+from bench import ClockSampler, kernel_traced, load_peaks, trace_efficiency  # noqa: E402
 from paper_2504_12526_b200 import _mom  # noqa: E402
 from paper_2504_12526_b200.stack import PrefillStack  # noqa: E402
 
@@ -81,6 +81,16 @@ def main():
             t = statistics.mean(per["lm_head_gemv"])
             out[mode]["lm_head_ms"] = t
             out[mode]["lm_head_gbs"] = V * d * 2 / (t * 1e-3) / 1e9
+        if mode == "offload_no_reload":
+            # one more step with in-kernel stamps: SM clock and MMA-issue efficiency per layer call
+            def traced():
+                with torch.cuda.stream(compute):
+                    x.copy_(x0)
+                    st.run(x, kv_fill, compute, copy)
+            M = -(-S // C)
+            t = kernel_traced(traced, (L - 1) * 2 * M + 4, dev)
+            out[mode]["kernel_trace"] = trace_efficiency(t, S, C, d, I,
+                                                         torch.cuda.get_device_properties(dev).multi_processor_count)
         del st
         torch.cuda.empty_cache()
     out["offload_overlap_ratio"] = out["offload_no_reload"]["ms_per_step"] / out["no_offload"]["ms_per_step"]
