@@ -36,6 +36,11 @@ def test_bench_single_gpu_contract(cuda_device):
     assert res["e2e"]["h2d_bytes_per_step"] > 0 and res["e2e"]["value"] > 0
     assert res["serial"]["value"] > 0
     assert res["activation_reduction_x"] > res["config"]["M"] * 0.99
+    kt = res["kernel_trace"]  # in-kernel timeline: clocks and MMA-issue efficiency are physical
+    assert "error" not in kt, kt
+    assert 500 < kt["phaseA_mhz"] <= res["clocks"]["sm_max_mhz"] + 50
+    assert 0.8 < kt["mlp_step_mma_issue_efficiency"] <= 1.02
+    assert kt["launches"] == 2 * 2 * res["config"]["M"]
 
 
 def test_bench_reference_arm():
