@@ -306,3 +306,25 @@ def test_norm_block_closed_forms():
     ref = oracle.mlp_rows(xn, x, wg, wu, wd, rows)
     got = oracle.mlp_norm_rows(x, gain, 1e-5, wg, wu, wd, rows)
     assert np.max(np.abs(got - ref)) <= 1e-6 * np.max(np.abs(ref))
+
+
+# ------------------------------------------------------------------ F1, property-based
+try:
+    from hypothesis import given, settings, strategies as st
+except ImportError:  # pragma: no cover
+    given = None
+
+if given is not None:
+    @settings(max_examples=40, deadline=None)
+    @given(S=st.integers(1, 40), C=st.integers(1, 50), d=st.integers(1, 9), I=st.integers(1, 11),
+           seed=st.integers(0, 10_000), residual=st.booleans())
+    def test_F1_property_any_partition(S, C, d, I, seed, residual):
+        """P:109-113 / P:286 for random shapes and partitions: mini-sequence output == unchunked output
+        bitwise, and any row subset (mlp_rows) equals the same rows of the full result bitwise."""
+        x = rng_f32((S, d), seed)
+        res = rng_f32((S, d), seed + 1) if residual else None
+        wg, wu, wd = rng_f32((I, d), seed + 2, 0.5), rng_f32((I, d), seed + 3, 0.5), rng_f32((d, I), seed + 4, 0.5)
+        ref = oracle.mlp_minseq(x, res, wg, wu, wd, C=S)
+        assert oracle.mlp_minseq(x, res, wg, wu, wd, C=C).tobytes() == ref.tobytes()
+        rows = sorted({(seed * 7 + k * 13) % S for k in range(min(S, 5))})
+        assert oracle.mlp_rows(x, res, wg, wu, wd, rows).tobytes() == ref[rows].tobytes()
