@@ -4,9 +4,18 @@ Tolerances (BASELINE.json north_star):
   * bf16 MLP outputs: max relative error <= 2e-2, read normwise:
         err = max|gpu - ref| / max|ref|, per tensor AND per row.
   * fp32 variants: the same metric <= 1e-4.
-  * last-token argmax: bit-exact (given the same hidden vector), with a tie guard:
-    when the oracle's top-2 gap is below the fp32 accumulation bound the test reports a
-    near-tie and accepts any index inside the bound instead of failing.
+  * bf16 regression bound (beside the 2e-2 gate): the tensor-level
+    normwise error must also stay <= REG_BF16 = 6e-3 at hidden >= 256.  Derivation: both sides
+    get the same bf16 inputs; the kernel rounds H_i once and each output once (RNE, relative
+    error <= 2^-9 = 1.95e-3 each) and accumulates in fp32 (K * 2^-24 ~ 1e-3 worst case at
+    K = 14336, ~1e-5 typical); the H rounding errors enter the down GEMM with random signs, so
+    they add ~2^-9/sqrt(3) of the row norm per output, a few sigma at the max.  6e-3 ~ 3 x 2^-9
+    is the sum of those terms with margin; a systematic error (a dropped K slice at d = 4096
+    removes 1/64 of the sum, ~1.6e-2) fails it while passing the 2e-2 gate.
+  * last-token argmax: bit-exact against the float64 oracle's argmax (given the same hidden
+    vector); every comparison logs the oracle's top-2 gap so a failure can be read as a near
+    tie or a real error.  Each gated comparison is recorded in RECORDS and printed in the
+    pytest terminal summary (tests/conftest.py).
 """
 from __future__ import annotations
 
@@ -14,6 +23,10 @@ import numpy as np
 
 TOL_BF16 = 2e-2
 TOL_F32 = 1e-4
+REG_BF16 = 6e-3
+
+# (kind, what, value, limit) of every comparison of this session; printed by conftest
+RECORDS: list = []
 
 
 def as_f64(a) -> np.ndarray:
@@ -43,25 +56,39 @@ def rowwise_err(got, ref) -> np.ndarray:
     return np.max(np.abs(got - ref), axis=1) / denom
 
 
-def check_close(got, ref, tol: float, what: str = "") -> float:
-    """Gate: normwise error per tensor and per row both <= tol.  Returns tensor error."""
+def check_close(got, ref, tol: float, what: str = "", regress: float | None = None) -> float:
+    """Gate: normwise error per tensor and per row both <= tol.  For bf16 (tol == TOL_BF16) with a
+    row length >= 256 the tensor error must also be <= REG_BF16 (pass regress=0 to skip, e.g. for
+    outputs that are not a single rounding of an fp32-accumulated value).  Returns tensor error."""
     e = normwise_err(got, ref)
     r = rowwise_err(got, ref)
     worst = int(np.argmax(r)) if r.size else -1
+    if regress is None:
+        n = as_f64(ref).shape[-1] if as_f64(ref).ndim else 1
+        regress = REG_BF16 if (tol == TOL_BF16 and n >= 256) else 0
+    RECORDS.append(("close", what, e, float(r.max()) if r.size else 0.0, tol, regress))
     assert e <= tol and (r.size == 0 or r.max() <= tol), (
         f"{what}: normwise err {e:.3e}, worst row {worst} err {r.max() if r.size else 0:.3e} > tol {tol:.1e}")
+    assert not regress or e <= regress, f"{what}: normwise err {e:.3e} > regression bound {regress:.1e}"
     return e
 
 
-def argmax_matches(gpu_idx: int, ref_logits, bound_rel: float = 1e-5) -> str:
-    """Returns "exact" when gpu_idx equals the oracle argmax (ties -> lowest index) or
-    "near-tie" when it differs but lies within the accumulation bound of the max.
-    Raises AssertionError otherwise."""
+def top2_gap(ref_logits) -> tuple[int, float, float]:
+    """(argmax with ties -> lowest index, top-1 minus top-2 logit, that gap / max|logit|)."""
     ref = as_f64(ref_logits).reshape(-1)
     best = int(np.argmax(ref))  # numpy argmax returns the first (lowest) index of the max
-    if gpu_idx == best:
-        return "exact"
-    bound = bound_rel * np.max(np.abs(ref))
-    assert 0 <= gpu_idx < ref.size and ref[best] - ref[gpu_idx] <= bound, (
-        f"argmax {gpu_idx} != oracle {best} (gap {ref[best] - ref[gpu_idx]:.3e} > {bound:.3e})")
-    return "near-tie"
+    if ref.size < 2:
+        return best, float("inf"), float("inf")
+    rest = np.delete(ref, best)
+    gap = float(ref[best] - rest.max())
+    return best, gap, gap / max(float(np.max(np.abs(ref))), 1e-300)
+
+
+def assert_argmax_exact(gpu_idx: int, ref_logits, what: str = "") -> float:
+    """Bit-exact argmax against the float64 oracle's logits; records and returns the
+    oracle's relative top-2 gap (the margin the kernel's fp32 accumulation had to respect)."""
+    best, gap, rel = top2_gap(ref_logits)
+    RECORDS.append(("argmax", what, float(rel), float(gap), gpu_idx, best))
+    assert gpu_idx == best, (f"{what}: argmax {gpu_idx} != oracle {best} (oracle top-2 gap {gap:.3e}, "
+                             f"{rel:.2e} of max|logit|)")
+    return rel

@@ -12,7 +12,7 @@ import oracle
 import synth
 from paper_2504_12526_b200 import _mom
 from paper_2504_12526_b200.stack import PrefillStack
-from tests.parity import TOL_BF16, argmax_matches, check_close
+from tests.parity import TOL_BF16, assert_argmax_exact, check_close
 
 pytestmark = pytest.mark.gpu
 
@@ -57,7 +57,7 @@ def _run_stack(cuda_device, d, I, V, L, S, C, d_kv, eps, check_layers, n_rows, o
     check_close(res.logits.cpu(), ref_logits, 1e-4, "LM head")
     am = int(res.argmax.item())
     assert am == oracle.argmax_f32(res.logits.cpu().numpy())
-    argmax_matches(am, ref_logits)
+    assert_argmax_exact(am, ref_logits, f"stack d={d} L={L} S={S} head")
     if offload:
         kv_rows = synth.sample_rows(S, C, n_random=max(8, S // 100))
         base_c = base.cpu()[kv_rows]

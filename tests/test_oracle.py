@@ -200,6 +200,14 @@ def test_rmsnorm_spec_worked_values():
     assert np.array_equal(oracle.rmsnorm(np.array(g["x"], float), None, g["eps"]), np.array(g["expect"], float))
     g = GOLD["rmsnorm_zero"]
     assert np.array_equal(oracle.rmsnorm(np.array(g["x"], float), None, g["eps"]), np.array(g["expect"], float))
+    # eps placement (eps inside the square root), with eps large enough that every other
+    # placement (outside the root, added to the rms, dropped) gives a different value
+    g = GOLD["rmsnorm_eps_inside"]
+    out = oracle.rmsnorm(np.array(g["x"], float), np.array(g["gain"], np.float32), g["eps"])
+    assert np.array_equal(out, np.array(g["expect"], float))
+    g = GOLD["rmsnorm_eps_34"]
+    out = oracle.rmsnorm(np.array(g["x"], float), None, g["eps"])
+    assert np.max(np.abs(out - np.array(g["expect"]))) < g["abs_tol"]
     # gain scales elementwise: [3,4] with gain [2, -1]
     out = oracle.rmsnorm(np.array([3.0, 4.0]), np.array([2.0, -1.0], np.float32), 0.0)
     assert np.max(np.abs(out - np.array([2 * 0.84852814, -1.13137085]))) < 1e-8
@@ -287,6 +295,26 @@ def test_norm_block_unit_rms_equals_plain_mlp():
     out = oracle.mlp_norm_rows(x, np.ones(d, np.float32), 0.0, wg, wu, wd, list(range(S)))
     ref = oracle.mlp_rows(x, x, wg, wu, wd, list(range(S)))
     assert out.tobytes() == ref.tobytes()
+
+
+SIGMA_HALF = 0.6224593312018546  # sigma(0.5) = 1 / (1 + e^-0.5), textbook value
+SIGMA_ONE = 0.7310585786300049   # sigma(1)
+
+
+def test_norm_block_eps_placement():
+    """S:126 eps inside the root, pinned through the f3 block (S:260 x + MLP(RMSNorm(x) * g)).
+    d = I = 2, identity weights, so out_c = x_c + xn_c * swish(xn_c) = x_c + xn_c^2 sigma(xn_c).
+    x = [1, 1], eps = 3 -> xn = [0.5, 0.5] (1/sqrt(1+3)); eps outside the root would give 0.25."""
+    eye = np.eye(2, dtype=np.float32)
+    x = np.array([[1.0, 1.0]], np.float32)
+    out = oracle.mlp_norm_rows(x, np.ones(2, np.float32), 3.0, eye, eye, eye, [0])[0]
+    assert np.max(np.abs(out - (1.0 + 0.25 * SIGMA_HALF))) < 1e-15
+    # gain 2 doubles xn to 1.0: out = 1 + sigma(1)
+    out = oracle.mlp_norm_rows(x, np.full(2, 2.0, np.float32), 3.0, eye, eye, eye, [0])[0]
+    assert np.max(np.abs(out - (1.0 + SIGMA_ONE))) < 1e-15
+    # eps = 0 on the same row: xn = x = 1 -> 1 + sigma(1)
+    out = oracle.mlp_norm_rows(x, np.ones(2, np.float32), 0.0, eye, eye, eye, [0])[0]
+    assert np.max(np.abs(out - (1.0 + SIGMA_ONE))) < 1e-15
 
 
 def test_norm_block_closed_forms():
