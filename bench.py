@@ -69,7 +69,15 @@ def parse_args():
                     help="request i+1 waits for request i's KV reload (no cross-request overlap)")
     ap.add_argument("--gather", choices=["fused", "nccl"], default="fused",
                     help="N>1: all-gather fused into the down-GEMM epilogue (f1) or a separate ncclAllGather")
-    return ap.parse_args()
+    ap.add_argument("--stack", action="store_true",
+                    help="whole layer stack (PrefillStack) of --config (default config 5: Llama-3-8B, 32 layers, "
+                         "S = 455000 tokens), token-sharded over the N ranks: strong scaling")
+    ap.add_argument("--layers", type=int, default=0,
+                    help="--stack: run only this many layers (test mode; the line says so)")
+    args = ap.parse_args()
+    if args.stack and "--config" not in sys.argv:
+        args.config = 4
+    return args
 
 
 # ----------------------------------------------------------------------------- distributed
@@ -706,6 +714,169 @@ def run_mine(args):
         dist.destroy_process_group()
 
 
+def verify_gathered_rows(st, x_full, weights, x_final, n_per_shard: int = 6):
+    """gather_verified: recompute sampled rows of EVERY rank's shard locally through the L-1
+    mini-sequence layers (mom_mlp_minseq_fwd on just those rows) and compare them bitwise with the
+    gathered final-layer input.  Rows are independent and the kernels' K order does not depend on
+    a row's position or on C (tested), so any difference is a transport / ordering error."""
+    from paper_2504_12526_b200 import _mom
+    g = torch.Generator().manual_seed(synth.SEED_ROWS + 7)
+    S_total = x_full.shape[0]
+    rows = set()
+    for r in range(st.world):
+        lo, hi = r * st.S, min(S_total, (r + 1) * st.S)
+        if lo >= hi:
+            continue
+        rows |= {lo, hi - 1}
+        rows |= set((lo + torch.randint(0, hi - lo, (n_per_shard,), generator=g)).tolist())
+    rows = sorted(rows)
+    xs = x_full[rows].clone()
+    for wg, wu, wd in weights[:-1]:
+        _mom.mlp_minseq_fwd(xs, xs, wg, wu, wd, xs, st.C)
+    torch.cuda.synchronize()
+    return bool(torch.equal(xs, x_final[rows])), len(rows)
+
+
+def run_stack(args):
+    """--stack: Alg. 1 over the whole layer stack of --config (default config 5, Llama-3-8B, 32 layers,
+    S = 455000 tokens), token-sharded over the N ranks: per layer each rank runs the
+    mini-sequence MLP on its S/N rows, offloads its K/V stand-in to its pinned host mirror, and gathers
+    the output rows into every rank's buffer (f1 peer stores + 1 NCCL barrier, or --gather nccl);
+    the rank owning the last token runs the final-layer GEMVs + LM head; every rank reloads its K/V.
+    Strong scaling: value = S_total / (max over ranks of the step time)."""
+    import psutil
+    from paper_2504_12526_b200 import _mom
+    from paper_2504_12526_b200 import build as _build
+    from paper_2504_12526_b200.stack import PrefillStack, shard_rows
+    world, rank, local = dist_setup(args)
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product has no CPU path)")
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    if not os.path.exists(_mom.LIB_PATH):
+        _build.build()
+    cfg = synth.CONFIGS[args.config]
+    peaks, peaks_src = load_peaks()
+    d, I, V, S_total, C = cfg.hidden, cfg.intermediate, cfg.vocab, cfg.S, cfg.C
+    L = args.layers or cfg.layers
+    start, per, padded = shard_rows(S_total, world, rank)
+    bf = torch.bfloat16
+    kv_shape = (per, 2 * cfg.d_kv)
+    host_need = L * per * 2 * cfg.d_kv * 2 * (world if SHARED_GPU else 1)
+    if psutil.virtual_memory().available < host_need * 1.15:
+        raise SystemExit(f"bench.py --stack: {host_need / 1e9:.1f} GB of pinned host memory needed for the "
+                         f"offloaded KV, {psutil.virtual_memory().available / 1e9:.1f} GB available (use --layers)")
+    comm = None
+    if world > 1 and not SHARED_GPU:
+        uid = _mom.nccl_get_unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        comm = _mom.nccl_comm_init(world, obj[0], rank)
+    gather = args.gather if world > 1 else "fused"
+    if SHARED_GPU and gather == "nccl":
+        raise SystemExit("bench.py --stack: --gather nccl needs one GPU per rank")
+    weights = [synth.mlp_weights(d, I, l, device, bf) for l in range(L)]
+    wh = synth.head_weight(V, d, device, bf)
+    gain = synth.norm_gain(d, device, bf)
+    x_full = synth.hidden(S_total, d, device, bf)     # the same global input at every N
+    x_mine = torch.zeros((per, d), dtype=bf, device=device)
+    n_real = max(0, min(per, S_total - start))
+    x_mine[:n_real] = x_full[start:start + n_real]
+    base = synth.kv_standin(per, cfg.d_kv, 0, device, bf)
+
+    def kv_fill(l, slot):  # attention stand-in (P:81): this rank's K/V rows of layer l
+        slot.copy_(base)
+
+    st = PrefillStack(weights, wh, gain, cfg.eps, per, C, kv_shape, device, world=world, rank=rank, comm=comm,
+                      S_total=S_total, gather=gather)
+    x_work = torch.empty_like(x_mine) if world == 1 else None
+    compute, copy = torch.cuda.Stream(device), torch.cuda.Stream(device)
+
+    def step(x_src=None, host=None):
+        with torch.cuda.stream(compute):
+            if world == 1:
+                if host is not None:
+                    x_work.copy_(host, non_blocking=True)
+                else:
+                    x_work.copy_(x_mine)
+                return st.run(x_work, kv_fill, compute, copy)
+            own = st.shard_of(st.xbuf[0])
+            own.copy_(host if host is not None else x_mine, non_blocking=True)
+            return st.run(own, kv_fill, compute, copy)
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+
+    def timed(n, host=None, sink=None):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(compute)
+        nl = 0
+        for _ in range(n):
+            r = step(host=host)
+            nl += r.launches
+            if sink is not None and r.logits is not None:
+                with torch.cuda.stream(compute):
+                    sink[0].copy_(r.logits, non_blocking=True)
+                    sink[1].copy_(r.argmax, non_blocking=True)
+        e1.record(compute)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / n, world, device), nl, r
+
+    with ClockSampler(device.index) as clk:
+        ms, n_launch, res = timed(args.steps)
+    flops = 6.0 * S_total * d * I * (L - 1)
+    ok, n_rows = verify_gathered_rows(st, x_full, weights, res.x_final)
+    ok_all = bool(sum_over_ranks(1.0 if ok else 0.0, world, device) == world)
+    burst = peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"])
+    sustained = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
+    tflops_per_gpu = flops / world / (ms * 1e-3) / 1e12
+    result = {
+        "metric": "prefill MLP tokens/s (MOM mini-sequence path over the layer stack, token-sharded)",
+        "value": S_total / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded random-init weights and inputs, synth/)",
+        "config": {"workload": cfg.name + ("" if L == cfg.layers else f"-first{L}layers"), "hidden": d,
+                   "intermediate": I, "vocab": V, "layers": L, "global_tokens": S_total, "tokens_per_rank": per,
+                   "minseq_len": C, "M_per_rank": -(-per // C), "parallelism": f"token-shard x{world}",
+                   "gather": gather if world > 1 else None,
+                   "barrier": ("nccl all-reduce" if comm is not None else "host (shared-GPU test mode)")
+                   if world > 1 else None,
+                   "kv_host_gb_per_rank": L * per * 2 * cfg.d_kv * 2 / 1e9,
+                   "l2": "inputs larger than L2 (x, weights, KV)"},
+        "mlp_tflops_per_gpu": tflops_per_gpu,
+        "mlp_frac_of_burst_per_gpu": tflops_per_gpu / burst,
+        "mlp_frac_of_sustained_per_gpu": tflops_per_gpu / sustained,
+        "note": "step time includes every layer's KV offload and the final reload (Alg. 1 P:106); the MLP "
+                "fraction divides the mini-sequence MLP FLOPs by the whole step time",
+        "gpu_launches": int(sum_over_ranks(n_launch, world, device)),
+        "gather_verified": ok_all, "gather_verified_rows_per_rank": n_rows,
+        "clocks": clk.summary(),
+        "shared_gpu_test_mode": SHARED_GPU or None,
+    }
+    if not args.no_e2e:
+        x_host = x_mine.cpu().pin_memory()
+        sink = (torch.empty(V, dtype=torch.float32, pin_memory=True), torch.empty(1, dtype=torch.int32,
+                                                                                 pin_memory=True))
+        e_ms, _, _ = timed(args.steps, host=x_host, sink=sink)
+        result["e2e"] = {"value": S_total / (e_ms * 1e-3), "unit": "tokens/s",
+                         "h2d_bytes_per_step": int(world * per * d * 2), "d2h_bytes_per_step": V * 4 + 4,
+                         "ms_per_step": e_ms}
+    st.close()
+    if comm is not None:
+        _mom.nccl_comm_destroy(comm)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def run_reference(args):
     """Reference arm: the CPU oracle (this paper-only tier's baseline) on the host cores."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -749,6 +920,8 @@ def main():
     args = parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.stack:
+        run_stack(args)
     else:
         run_mine(args)
 

@@ -6,11 +6,19 @@ Pure control flow around the C-ABI calls (no arithmetic of the method runs here)
      finished -- event-gated, so the caching allocator never recycles memory under a live copy);
   2. mom_kv_offload copies it to the pinned host mirror of layer l on the copy stream,
      overlapping the MLP;
-  3. non-final layers: mom_mlp_minseq_fwd in place, x <- x + MLP(x), and, when the
-     tokens are sharded over N GPUs, mom_allgather_rows rebuilds the [N*S, d] rows;
-  4. final layer: mom_mlp_last_token on the last token (P:102-103), mom_lm_head_last (P:105);
+  3. non-final layers: mom_mlp_minseq_fwd, x <- x + MLP(x).  One GPU: in place.
+     Token-sharded over N GPUs: every rank holds the [N*S_r, d] rows in
+     TWO gathered buffers used alternately -- layer l reads buffer l % 2 and writes its output rows
+     into buffer (l+1) % 2 of every rank (f1: the phase-B epilogue stores them to the IPC-mapped
+     peer buffers; or mom_allgather_rows, the NCCL baseline), then one barrier per layer
+     (mom_nccl_barrier, or a host barrier in the one-GPU test mode).  Because no rank starts
+     layer l+1 before every rank finished layer l, nothing a rank may still read in buffer l % 2
+     (its MLP input; a full model's attention over all rows) is overwritten while it is read;
+  4. final layer: mom_mlp_last_token on the last token, mom_lm_head_last on
+     the rank that owns token S_total - 1;
   5. after the head, mom_kv_reload brings every layer's K/V back to the device, one
-     event per layer (f4: a decode step may start layer l as soon as its K/V is back).
+     event per layer (f4: a decode step may start layer l as soon as its K/V is back; see
+     decode_consumer_pass).
 Token sharding: rank r owns rows [r*S_r, (r+1)*S_r) of N*S_r (padded) rows.
 """
 from __future__ import annotations
@@ -38,6 +46,11 @@ def last_token_owner(S_total: int, world: int) -> int:
     return (S_total - 1) // per
 
 
+def gathered_buffer_index(layer: int) -> int:
+    """Token-sharded stacks: layer l reads gathered buffer l % 2 and writes buffer (l+1) % 2."""
+    return layer % 2
+
+
 @dataclass
 class StackResult:
     y_last: torch.Tensor | None
@@ -49,24 +62,36 @@ class StackResult:
     # f4: one event per layer, recorded on the copy stream when that layer's K/V is back on the
     # device; a decode step can start layer l after reload_done[l] while layers > l still stream
     reload_done: list = field(default_factory=list)
+    # the final layer's input rows (all N*S_r rows when token-sharded; x itself on one GPU)
+    x_final: torch.Tensor | None = None
+    copy_stream: torch.cuda.Stream | None = None
 
 
 class PrefillStack:
-    """MOM prefill of the MLP path over L layers on one GPU (or one token shard of N)."""
+    """MOM prefill of the MLP path over L layers on one GPU (or one token shard of N).
+
+    Token-sharded (world > 1): `gather` = "fused" maps every peer's two gathered buffers through
+    cudaIpc handles exchanged over `group` (torch.distributed) and stores the output rows there from
+    the MLP kernels; "nccl" runs mom_allgather_rows after each layer (needs one GPU per rank).
+    The per-layer barrier is mom_nccl_barrier on `comm`, or, when comm is None (the one-GPU test
+    mode with several ranks on one device), a host barrier over `group`."""
 
     def __init__(self, weights, w_head, norm_gain, eps, S_local, minseq_len, kv_shape, device,
-                 world=1, rank=0, comm=None, S_total=None, offload=True, reload=True, peers=None,
-                 pipelined_reload=False):
+                 world=1, rank=0, comm=None, S_total=None, offload=True, reload=True, gather="fused",
+                 group=None, pipelined_reload=False):
         self.weights = weights            # list of (w_gate, w_up, w_down), layer 0..L-1
         self.L = len(weights)
         self.wh, self.gain, self.eps = w_head, norm_gain, eps
         self.S, self.C = S_local, minseq_len
-        self.world, self.rank, self.comm = world, rank, comm
-        # f1: peers' x buffers (NVLink-mapped, offset to this rank's shard rows); the phase-B
-        # epilogue stores every output row there, so no separate all-gather runs
-        self.peers = list(peers or [])
-        self.barrier_scratch = torch.zeros(1, dtype=torch.int32, device=device) if world > 1 else None
+        self.world, self.rank, self.comm, self.group = world, rank, comm, group
+        if gather not in ("fused", "nccl"):
+            raise ValueError("gather must be 'fused' or 'nccl'")
+        if world > 1 and gather == "nccl" and comm is None:
+            raise ValueError("gather='nccl' needs an NCCL communicator")
+        self.gather = gather
         self.S_total = S_total if S_total is not None else S_local * world
+        if world > 1 and not (world - 1) * S_local < self.S_total <= world * S_local:
+            raise ValueError("S_total must satisfy (world-1)*S_local < S_total <= world*S_local")
         self.device = device
         wg0 = weights[0][0]
         self.dtype = wg0.dtype
@@ -89,18 +114,75 @@ class PrefillStack:
         self.logits = torch.empty(self.V, dtype=torch.float32, device=device)
         self.argmax = torch.empty(1, dtype=torch.int32, device=device)
         self.owner = last_token_owner(self.S_total, world)
+        # the previous run's copies (offload into kv_host, reload out of it) must finish before a new
+        # run refills the ring and the host mirrors (pipelined_reload leaves them in flight)
+        self._prev_copies_done = None
+        self.xbuf, self.peers, self._peer_maps = [], [[], []], []
+        if world > 1:
+            self.barrier_scratch = torch.zeros(1, dtype=torch.int32, device=device)
+            self.xbuf = [torch.zeros((world * S_local, self.d), dtype=self.dtype, device=device) for _ in range(2)]
+            if gather == "fused":
+                self._map_peers()
 
+    # ---------------------------------------------------------------- token-sharded plumbing
+    def _map_peers(self):
+        """Exchange the cudaIpc handles of both gathered buffers and map every peer's, offset to this
+        rank's shard rows (where this rank's phase-B epilogue stores its output rows)."""
+        import torch.distributed as dist
+        mine = [_mom.ipc_get_handle(b) for b in self.xbuf]
+        handles = [None] * self.world
+        dist.all_gather_object(handles, mine, group=self.group)
+        shard_off = self.rank * self.S * self.d * self.xbuf[0].element_size()
+        for b in range(2):
+            for r in range(self.world):
+                if r == self.rank:
+                    continue
+                h, off = handles[r][b]
+                ptr = _mom.ipc_open_handle(h, off)
+                self._peer_maps.append((ptr, off))
+                self.peers[b].append(ptr + shard_off)
+
+    def close(self):
+        """Unmap the peers' buffers (collective: every rank calls it after its last run)."""
+        if self._peer_maps:
+            import torch.distributed as dist
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=self.group)  # no peer still stores into our buffers
+            for ptr, off in self._peer_maps:
+                _mom.ipc_close(ptr, off)
+            self._peer_maps, self.peers = [], [[], []]
+
+    def _barrier(self, stream):
+        if self.comm is not None:
+            _mom.nccl_barrier(self.comm, self.barrier_scratch, stream)
+        else:  # one-GPU test mode (several ranks on one device, gloo): host barrier
+            import torch.distributed as dist
+            stream.synchronize()
+            dist.barrier(group=self.group)
+
+    def shard_of(self, buf):
+        return buf[self.rank * self.S:(self.rank + 1) * self.S]
+
+    # ---------------------------------------------------------------- one prefill request
     def run(self, x, kv_fill=None, compute=None, copy=None, on_layer=None):
-        """x: [world * S_local, d] device tensor (this rank's shard at rows rank*S_local), updated in
-        place to the final layer's input.  kv_fill(l, slot) writes layer l's stand-in K/V on the
-        current stream.  on_layer(l, x) is called (host side, after enqueueing) before layer l's MLP
-        -- tests use it to snapshot teacher-forcing inputs.  Returns a StackResult."""
+        """One GPU: x is [S, d], updated in place to the final layer's input.  Token-sharded: x is
+        this rank's [S_local, d] input rows, or a [world * S_local, d] tensor holding them at rows
+        rank*S_local (copied into gathered buffer 0 unless x is that buffer).  kv_fill(l, slot)
+        writes layer l's stand-in K/V on the current stream.  on_layer(l, buf) is called (host side,
+        after enqueueing) before layer l's MLP with the buffer holding layer l's input -- tests use
+        it to snapshot teacher-forcing inputs.  Returns a StackResult."""
         compute = compute or torch.cuda.current_stream(self.device)
         copy = copy or torch.cuda.Stream(self.device)
         ev_off = [torch.cuda.Event() for _ in range(self.L)]
-        shard = x[self.rank * self.S:(self.rank + 1) * self.S]
         launches = 0
         with torch.cuda.stream(compute):
+            if self._prev_copies_done is not None:
+                compute.wait_event(self._prev_copies_done)
+            if self.world > 1:
+                own = self.shard_of(self.xbuf[0])
+                src = x if x.shape[0] == self.S else self.shard_of(x)
+                if src.data_ptr() != own.data_ptr():
+                    own.copy_(src)
             for l in range(self.L):
                 if self.offload:
                     slot = self.kv_ring[l % 2]
@@ -109,25 +191,32 @@ class PrefillStack:
                     if kv_fill is not None:
                         kv_fill(l, slot)
                     _mom.kv_offload(slot, self.kv_host[l], compute, copy, ev_off[l])          # a9
+                cur = x if self.world == 1 else self.xbuf[gathered_buffer_index(l)]
                 if on_layer is not None:
-                    on_layer(l, x)
+                    on_layer(l, cur)
                 wg, wu, wd = self.weights[l]
                 if l < self.L - 1:
-                    if self.world > 1 and self.peers:  # a1-a5 + a11 fused (f1)
-                        _mom.mlp_minseq_fwd_gather(shard, shard, wg, wu, wd, shard, self.peers, self.C, self.ws,
-                                                   compute)
-                        _mom.nccl_barrier(self.comm, self.barrier_scratch, compute)
+                    if self.world == 1:
+                        _mom.mlp_minseq_fwd(x, x, wg, wu, wd, x, self.C, self.ws, compute)          # a1-a5
                     else:
-                        _mom.mlp_minseq_fwd(shard, shard, wg, wu, wd, shard, self.C, self.ws, compute)  # a1-a5
-                        if self.world > 1:
-                            _mom.allgather_rows(x, self.S, self.comm, self.rank, self.world, compute)  # a11
+                        nxt_i = gathered_buffer_index(l + 1)
+                        src, dst = self.shard_of(cur), self.shard_of(self.xbuf[nxt_i])
+                        if self.gather == "fused":                                                 # a11 fused (f1)
+                            _mom.mlp_minseq_fwd_gather(src, src, wg, wu, wd, dst, self.peers[nxt_i], self.C,
+                                                       self.ws, compute)
+                            self._barrier(compute)
+                        else:
+                            _mom.mlp_minseq_fwd(src, src, wg, wu, wd, dst, self.C, self.ws, compute)
+                            _mom.allgather_rows(self.xbuf[nxt_i], self.S, self.comm, self.rank, self.world,
+                                                compute)                                           # a11 (NCCL)
                     launches += 2 * math.ceil(self.S / self.C)
                 elif self.rank == self.owner:
-                    last = x[self.S_total - 1]
+                    last = cur[self.S_total - 1]
                     _mom.mlp_last_token(last, last, wg, wu, wd, self.y, self.ws_last, compute)     # a6
                     _mom.lm_head_last(self.y, self.gain, self.eps, self.wh, self.logits, self.argmax,
                                       self.ws_head, compute)                                       # a7-a8
                     launches += 4
+            x_final = x if self.world == 1 else self.xbuf[gathered_buffer_index(self.L - 1)]
             reload_done = []
             if self.reload:
                 copy.wait_stream(compute)  # Alg. 1: after the head
@@ -135,8 +224,11 @@ class PrefillStack:
                     ev = torch.cuda.Event()
                     _mom.kv_reload(self.kv_host[l], self.kv_dev[l], copy, ev)                      # a10
                     reload_done.append(ev)
-                if not self.pipelined_reload:
-                    compute.wait_stream(copy)
+            done = torch.cuda.Event()
+            done.record(copy)
+            self._prev_copies_done = done
+            if not self.pipelined_reload:
+                compute.wait_stream(copy)
         own = self.rank == self.owner
         return StackResult(self.y if own else None, self.logits if own else None, self.argmax if own else None,
-                           self.kv_host, self.kv_dev, launches, reload_done)
+                           self.kv_host, self.kv_dev, launches, reload_done, x_final, copy)
