@@ -98,6 +98,33 @@ def dist_setup(args):
     return world, rank, local
 
 
+def init_nccl(world: int, rank: int) -> int:
+    """NCCL communicator of the library (rank 0's unique id broadcast over torch.distributed)."""
+    from paper_2504_12526_b200 import _mom
+    uid = _mom.nccl_get_unique_id() if rank == 0 else bytes(128)
+    obj = [uid]
+    dist.broadcast_object_list(obj, src=0)
+    comm = _mom.nccl_comm_init(world, obj[0], rank)
+    n = _mom.nccl_comm_count(comm)
+    if n != world:
+        raise SystemExit(f"bench.py: NCCL communicator has {n} ranks, expected {world}")
+    return comm
+
+
+def try_collective(fn, world: int, device):
+    """Run fn() on every rank; returns None if it succeeded everywhere, else the first failure's
+    reason (every rank learns that some rank failed, so all take the same fallback)."""
+    why = None
+    try:
+        fn()
+    except Exception as e:  # noqa: BLE001 -- the reason is reported in the JSON line
+        why = f"{type(e).__name__}: {e}"[:300]
+    reasons = [None] * world
+    dist.all_gather_object(reasons, why)
+    bad = [r for r in reasons if r is not None]
+    return bad[0] if bad else None
+
+
 def _reduce(x: float, world: int, device, op) -> float:
     if world == 1:
         return x
@@ -237,7 +264,15 @@ class Workload:
         """Exchange cudaIpcMemHandles of every rank's gathered buffer and map the peers'."""
         from paper_2504_12526_b200 import _mom
         handles = [None] * self.world
-        dist.all_gather_object(handles, _mom.ipc_get_handle(self.out))
+        try:
+            mine = _mom.ipc_get_handle(self.out)
+        except Exception as e:  # noqa: BLE001 -- every rank must reach the all_gather below
+            mine = e
+        dist.all_gather_object(handles, mine if not isinstance(mine, Exception) else None)
+        if isinstance(mine, Exception):
+            raise mine
+        if any(h is None for h in handles):
+            raise RuntimeError("a peer could not export its gathered buffer (cudaIpcGetMemHandle)")
         row_bytes = self.d * 2
         for r in range(self.world):
             if r != self.rank:
@@ -510,16 +545,23 @@ def run_mine(args):
     cfg = synth.CONFIGS[args.config]
     peaks, peaks_src = load_peaks()
     wl = Workload(cfg, rank, world, device)
+    dist_info = {}
     if world > 1:
         if not SHARED_GPU:
-            uid = _mom.nccl_get_unique_id() if rank == 0 else bytes(128)
-            obj = [uid]
-            dist.broadcast_object_list(obj, src=0)
-            wl.comm = _mom.nccl_comm_init(world, obj[0], rank)
+            wl.comm = init_nccl(world, rank)
+            dist_info["nccl_comm_nranks"] = _mom.nccl_comm_count(wl.comm)
         elif args.gather != "fused":
             args.no_e2e = True  # the NCCL all-gather needs one GPU per rank
         if args.gather == "fused":
-            wl.map_peers()
+            why = try_collective(lambda: wl.map_peers(), world, device)
+            if why is not None:  # e.g. expandable_segments memory cannot be IPC-exported
+                wl.unmap_peers()
+                if wl.comm is None:
+                    raise SystemExit(f"bench.py: fused gather unavailable ({why}) and no NCCL fallback in "
+                                     "shared-GPU mode")
+                args.gather = "nccl"
+                dist_info["gather_fallback_reason"] = why
+        dist_info["gather"] = args.gather
     compute = torch.cuda.Stream(device)
     copy = torch.cuda.Stream(device)
     reload = torch.cuda.Stream(device)
@@ -716,6 +758,10 @@ def run_mine(args):
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(wl)
+    if wl.comm is not None:
+        _mom.nccl_check(wl.comm)  # raises if any collective of the run left the communicator in error
+    if dist_info:
+        result["distributed"] = dist_info
     if wl.peer_maps:
         torch.cuda.synchronize()
         dist.barrier()
@@ -782,11 +828,10 @@ def run_stack(args):
         raise SystemExit(f"bench.py --stack: {host_need / 1e9:.1f} GB of pinned host memory needed for the "
                          f"offloaded KV, {psutil.virtual_memory().available / 1e9:.1f} GB available (use --layers)")
     comm = None
+    dist_info = {}
     if world > 1 and not SHARED_GPU:
-        uid = _mom.nccl_get_unique_id() if rank == 0 else bytes(128)
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        comm = _mom.nccl_comm_init(world, obj[0], rank)
+        comm = init_nccl(world, rank)
+        dist_info["nccl_comm_nranks"] = _mom.nccl_comm_count(comm)
     gather = args.gather if world > 1 else "fused"
     if SHARED_GPU and gather == "nccl":
         raise SystemExit("bench.py --stack: --gather nccl needs one GPU per rank")
@@ -802,8 +847,23 @@ def run_stack(args):
     def kv_fill(l, slot):  # attention stand-in: this rank's K/V rows of layer l
         slot.copy_(base)
 
-    st = PrefillStack(weights, wh, gain, cfg.eps, per, C, kv_shape, device, world=world, rank=rank, comm=comm,
-                      S_total=S_total, gather=gather)
+    st = None
+    if world > 1 and gather == "fused":
+        box = []
+        why = try_collective(lambda: box.append(PrefillStack(weights, wh, gain, cfg.eps, per, C, kv_shape, device,
+                                                             world=world, rank=rank, comm=comm, S_total=S_total,
+                                                             gather="fused")), world, device)
+        if why is None:
+            st = box[0]
+        else:
+            if box:
+                box[0].close(barrier=False)
+            if comm is None:
+                raise SystemExit(f"bench.py --stack: fused gather unavailable ({why}), no NCCL in shared-GPU mode")
+            gather, dist_info["gather_fallback_reason"] = "nccl", why
+    if st is None:
+        st = PrefillStack(weights, wh, gain, cfg.eps, per, C, kv_shape, device, world=world, rank=rank, comm=comm,
+                          S_total=S_total, gather=gather)
     x_work = torch.empty_like(x_mine) if world == 1 else None
     compute, copy = torch.cuda.Stream(device), torch.cuda.Stream(device)
 
@@ -882,6 +942,10 @@ def run_stack(args):
         result["e2e"] = {"value": S_total / (e_ms * 1e-3), "unit": "tokens/s",
                          "h2d_bytes_per_step": int(world * per * d * 2), "d2h_bytes_per_step": V * 4 + 4,
                          "ms_per_step": e_ms}
+    if comm is not None:
+        _mom.nccl_check(comm)
+    if dist_info:
+        result["distributed"] = dist_info
     st.close()
     if comm is not None:
         _mom.nccl_comm_destroy(comm)

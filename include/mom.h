@@ -31,7 +31,9 @@
  *               mini-sequences) stay enqueued.  mom_last_error() returns a thread-local message.
  *   Tuning      Environment knobs read per call (defaults are the measured best on B200):
  *               MOM_CTA_GROUP (2), MOM_GROUP_M_A (16), MOM_GROUP_M_B (8), MOM_TMA_POLICY (0),
- *               MOM_FUSED (0: two launches per mini-sequence), MOM_EPI_A_COALESCED (1),
+ *               MOM_FUSED (0: two launches per mini-sequence; 1: one persistent launch whose grid
+ *               is clamped to cudaOccupancyMaxActiveClusters, since its phase-B tiles wait on
+ *               phase-A tiles of other clusters), MOM_EPI_A_COALESCED (1),
  *               MOM_GATHER_FORWARD (1: f1 rows of mini-sequence i-1 forwarded during i),
  *               MOM_GEMV_PDL (1), MOM_GEMV_VARIANT (1: down GEMV with 4 loads in flight per
  *               row at 2 blocks/SM; 0: the earlier 2 at 4/SM), MOM_MLP_PDL (1: programmatic dependent launch between the
@@ -242,7 +244,12 @@ mom_status_t mom_nccl_barrier(void *comm, int32_t *scratch /* device int32[1] */
  * the peers' gathered [N*S_local, hidden] buffers at this rank's shard, NVLink-mapped with
  * mom_ipc_open_handle.  The rows cross NVLink while the tensor cores keep working, instead
  * of in a separate collective after the layer.  After the call, one mom_nccl_barrier on
- * the same stream orders every rank's peer stores before any rank's next layer.
+ * the same stream guarantees that every rank's peer stores of THIS call have landed before any
+ * rank runs past the barrier.  It does not protect a reader of the destination rows from the
+ * stores of a LATER call: a caller whose ranks read the gathered rows while the next layer runs
+ * (a full model's attention over all rows) must alternate two gathered buffers, layer l writing
+ * buffer (l+1) % 2 -- then the barrier of layer l, which every rank passes only after its own
+ * layer-l work, orders all reads of a buffer before the next stores into it (stack.py does this).
  *   0 <= n_peers <= 7; peer_out[k] 16-B aligned; bf16 only when n_peers > 0.
  * IPC plumbing: mom_ipc_get_handle returns the 64-byte cudaIpcMemHandle of the allocation
  * holding dev_ptr and dev_ptr's offset in it (torch sub-allocates); mom_ipc_open_handle maps
@@ -270,6 +277,17 @@ mom_status_t mom_ipc_close(void *dev_ptr, int64_t offset);
 mom_status_t mom_nccl_get_unique_id(void *id_out /* 128 bytes */);
 mom_status_t mom_nccl_comm_init(void **comm_out, int nranks, const void *id /* 128 B */, int rank);
 mom_status_t mom_nccl_comm_destroy(void *comm);
+/* Failure detection.  Every NCCL-issuing entry (mom_allgather_rows, mom_nccl_barrier,
+ * mom_argmax_allreduce) polls ncclCommGetAsyncError after enqueueing and returns MOM_ERR_NCCL if the
+ * communicator is in an error state (a failed or aborted peer, an error inside an earlier collective).
+ *   mom_nccl_check        the same poll, host-side and non-blocking: a caller waiting on a stream that
+ *                         holds collectives calls it periodically; MOM_OK while healthy
+ *                         (ncclSuccess / ncclInProgress), MOM_ERR_NCCL with the NCCL reason otherwise.
+ *   mom_nccl_comm_count   *nranks_out = ncclCommCount(comm) (confirms the world size after init).
+ *   mom_nccl_comm_abort   ncclCommAbort: unblocks collectives stuck on a dead peer; the comm is freed. */
+mom_status_t mom_nccl_check(void *comm);
+mom_status_t mom_nccl_comm_count(void *comm, int *nranks_out);
+mom_status_t mom_nccl_comm_abort(void *comm);
 mom_status_t mom_allgather_rows(void *rows, int64_t rows_per_rank, int64_t hidden, mom_dtype_t dt,
                                 void *comm, int rank, int nranks, mom_stream_t stream);
 
@@ -293,7 +311,8 @@ mom_status_t mom_set_timing_events(mom_event_t *events, int32_t *kinds, int64_t 
  * 2 last MMA issued (leader CTAs), 3 CTA exit; the SM's clock64 at k = 4 first and 5 last MMA
  * (so the SM clock over the launch is (k5 - k4) / (k2 - k1)); k = 6 the SM cycles epilogue warp 4
  * spent in tile epilogues (summed), k = 7 their count; *count is incremented per launch.
- * dev_buf: device uint64[capacity * 160 * 8], zeroed by the caller.  NULL disables. */
+ * dev_buf: device uint64[capacity * 160 * 8], zeroed by the caller.  NULL disables.  A launch whose
+ * persistent grid exceeds 160 CTAs (a part with more than 160 SMs) is not traced (no slot used). */
 mom_status_t mom_set_kernel_trace(void *dev_buf, int64_t capacity, int64_t *count);
 
 #ifdef __cplusplus

@@ -41,6 +41,9 @@ SIGNATURES = {
     "mom_nccl_get_unique_id": (_i32, [_p]),
     "mom_nccl_comm_init": (_i32, [ctypes.POINTER(ctypes.c_void_p), _i32, _p, _i32]),
     "mom_nccl_comm_destroy": (_i32, [_p]),
+    "mom_nccl_check": (_i32, [_p]),
+    "mom_nccl_comm_count": (_i32, [_p, ctypes.POINTER(ctypes.c_int)]),
+    "mom_nccl_comm_abort": (_i32, [_p]),
     "mom_allgather_rows": (_i32, [_p, _i64, _i64, _i32, _p, _i32, _i32, _p]),
     "mom_set_timing_events": (_i32, [_p, _p, _i64, _p]),
     "mom_set_kernel_trace": (_i32, [_p, _i64, ctypes.POINTER(ctypes.c_int64)]),
@@ -258,6 +261,7 @@ def fold_norm_gain(w, norm_gain, w_folded=None, stream=None):
 def mlp_minseq_rmsnorm_fwd(x, w_gate_folded, w_up_folded, w_down, out, minseq_len: int, eps: float,
                            workspace=None, stream=None):
     """f3: out = x + MLP(RMSNorm(x) * g) with g folded into W_gate/W_up, per mini-sequence."""
+    _check_mlp(x, None, w_gate_folded, w_up_folded, w_down, out)
     S, hidden = x.shape
     I = w_gate_folded.shape[0]
     dt = _dt(x)
@@ -307,6 +311,11 @@ def lm_head_shard(h_last, norm_gain, eps: float, w_head_shard, vocab_offset: int
     """f2: this rank's vocab shard of the LM head; best_key (device int64[1]) gets the packed best."""
     hidden = h_last.shape[-1]
     Vs = w_head_shard.shape[0]
+    _expect("h_last", h_last, (hidden,), h_last.dtype)
+    _expect("norm_gain", norm_gain, (hidden,), h_last.dtype)
+    _expect("w_head_shard", w_head_shard, (Vs, hidden), h_last.dtype)
+    _expect("logits_shard", logits_shard, (Vs,), torch.float32)
+    _expect("best_key", best_key, (1,), torch.int64)
     if workspace is None:
         workspace = torch.empty(lib().mom_lm_head_workspace_bytes(Vs), dtype=torch.uint8, device=h_last.device)
     _check(lib().mom_lm_head_shard(_ptr(h_last), _ptr(norm_gain), float(eps), _ptr(w_head_shard), vocab_offset, Vs,
@@ -321,9 +330,19 @@ def argmax_allreduce(best_key, argmax, comm=None, stream=None):
     return argmax
 
 
+def _copy_bytes(kv_dev, kv_host, nbytes, what) -> int:
+    """Bytes of a KV copy: nbytes (default: all of kv_dev); both buffers must hold at least that."""
+    dev_b = kv_dev.numel() * kv_dev.element_size()
+    host_b = kv_host.numel() * kv_host.element_size()
+    n = dev_b if nbytes is None else int(nbytes)
+    if n < 0 or n > dev_b or n > host_b:
+        raise ValueError(f"{what}: {n} bytes requested, device buffer {dev_b} B, host buffer {host_b} B")
+    return n
+
+
 def kv_offload(kv_dev, kv_host_pinned, producer_stream=None, copy_stream=None, done=None, nbytes=None):
     """Alg. 1: async D2H of one layer's K/V into pinned host memory on copy_stream."""
-    n = nbytes if nbytes is not None else kv_dev.numel() * kv_dev.element_size()
+    n = _copy_bytes(kv_dev, kv_host_pinned, nbytes, "kv_offload")
     ev = _event_handle(done)
     _check(lib().mom_kv_offload(_ptr(kv_dev), _ptr(kv_host_pinned), n, _stream(producer_stream),
                                 _stream(copy_stream), ev))
@@ -334,7 +353,7 @@ def kv_offload(kv_dev, kv_host_pinned, producer_stream=None, copy_stream=None, d
 
 def kv_reload(kv_host_pinned, kv_dev, copy_stream=None, done=None, nbytes=None):
     """Alg. 1: async H2D of the offloaded cache before decode."""
-    n = nbytes if nbytes is not None else kv_dev.numel() * kv_dev.element_size()
+    n = _copy_bytes(kv_dev, kv_host_pinned, nbytes, "kv_reload")
     ev = _event_handle(done)
     _check(lib().mom_kv_reload(_ptr(kv_host_pinned), _ptr(kv_dev), n, _stream(copy_stream), ev))
     if done is not None and ev is None:
@@ -423,9 +442,27 @@ def nccl_comm_destroy(comm: int):
     _check(lib().mom_nccl_comm_destroy(comm))
 
 
+def nccl_check(comm: int):
+    """Raises MomError(MOM_ERR_NCCL) if the communicator is in an error state (non-blocking poll)."""
+    _check(lib().mom_nccl_check(comm))
+
+
+def nccl_comm_count(comm: int) -> int:
+    n = ctypes.c_int(0)
+    _check(lib().mom_nccl_comm_count(comm, ctypes.byref(n)))
+    return n.value
+
+
+def nccl_comm_abort(comm: int):
+    _check(lib().mom_nccl_comm_abort(comm))
+
+
 def allgather_rows(rows, rows_per_rank: int, comm: int, rank: int, nranks: int, stream=None):
     """In-place all-gather of every rank's [rows_per_rank, hidden] shard of `rows`."""
     hidden = rows.shape[-1]
+    if rows.dim() != 2 or rows.shape[0] < nranks * rows_per_rank:
+        raise ValueError(f"allgather_rows: rows must be [>= {nranks} * {rows_per_rank}, hidden], "
+                         f"got {tuple(rows.shape)}")
     _check(lib().mom_allgather_rows(_ptr(rows), rows_per_rank, hidden, _dt(rows), comm, rank, nranks,
                                     _stream(stream)))
     return rows

@@ -115,8 +115,10 @@ struct TraceHook {
   int64_t *count = nullptr;
 };
 thread_local TraceHook g_trace;
-unsigned long long *next_trace_slot() {
+unsigned long long *next_trace_slot(int grid_ctas) {
+  // a slot holds kMaxTraceCtas CTAs x 8 stamps: a larger persistent grid is not traced
   if (!g_trace.buf || !g_trace.count || *g_trace.count >= g_trace.cap) return nullptr;
+  if (grid_ctas > static_cast<int>(mom::kMaxTraceCtas)) return nullptr;
   return g_trace.buf + (*g_trace.count)++ * (mom::kMaxTraceCtas * 8);
 }
 
@@ -401,7 +403,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
       if (e != cudaSuccess) return cuda_fail(e, "counter reset");
       a.group_m = group_a;
       ScopedTiming tm(stream, 6);
-      a.trace = next_trace_slot();
+      a.trace = next_trace_slot(num_sms);
       e = mom::launch_mlp_tc(a, 2, stream);
       if (e != cudaSuccess) return cuda_fail(e, "fused MLP (tcgen05)");
       continue;
@@ -413,7 +415,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     a.pdl = mlp_pdl && i > 0 && !x_host;
     {
       ScopedTiming tm(stream, 0);
-      a.trace = next_trace_slot();
+      a.trace = next_trace_slot(num_sms);
       e = mom::launch_mlp_tc(a, 0, stream);  // H_i = Swish(A_i Wg^T) (.) A_i Wu^T
     }
     if (e != cudaSuccess) return cuda_fail(e, "phase A (tcgen05)");
@@ -423,7 +425,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     a.pdl = mlp_pdl;
     {
       ScopedTiming tm(stream, 1);
-      a.trace = next_trace_slot();
+      a.trace = next_trace_slot(num_sms);
       e = mom::launch_mlp_tc(a, 1, stream);  // O_i = R_i + H_i Wd^T, written at rows r0..
     }
     if (e != cudaSuccess) return cuda_fail(e, "phase B (tcgen05)");
@@ -486,7 +488,9 @@ mom_status_t mom_ipc_get_handle(const void *dev_ptr, void *handle_out, int64_t *
     return fail(MOM_ERR_INVALID_ARG, "mom_ipc_get_handle: not a device allocation");
   cudaIpcMemHandle_t h;
   cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base));
-  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  if (e != cudaSuccess)
+    return cuda_fail(e, "cudaIpcGetMemHandle (the allocation is not IPC-exportable -- e.g. torch's "
+                        "expandable_segments / cuMemCreate memory; use the NCCL all-gather path)");
   memcpy(handle_out, &h, sizeof(h));
   *offset_out = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
   return MOM_OK;
@@ -785,8 +789,14 @@ typedef int (*nccl_destroy_fn)(void *);
 typedef int (*nccl_allgather_fn)(const void *, void *, size_t, int, void *, cudaStream_t);
 typedef int (*nccl_allreduce_fn)(const void *, void *, size_t, int, int, void *, cudaStream_t);
 typedef const char *(*nccl_errstr_fn)(int);
+typedef int (*nccl_async_err_fn)(void *, int *);
+typedef int (*nccl_count_fn)(void *, int *);
+typedef int (*nccl_abort_fn)(void *);
 struct Nccl {
   bool ok = false;
+  nccl_async_err_fn async_err = nullptr;  // ncclCommGetAsyncError
+  nccl_count_fn count = nullptr;          // ncclCommCount
+  nccl_abort_fn abort = nullptr;          // ncclCommAbort
   nccl_get_uid_fn get_uid = nullptr;
   nccl_init_fn init = nullptr;
   nccl_destroy_fn destroy = nullptr;
@@ -811,7 +821,10 @@ Nccl &nccl() {
     n.allgather = reinterpret_cast<nccl_allgather_fn>(dlsym(h, "ncclAllGather"));
     n.allreduce = reinterpret_cast<nccl_allreduce_fn>(dlsym(h, "ncclAllReduce"));
     n.errstr = reinterpret_cast<nccl_errstr_fn>(dlsym(h, "ncclGetErrorString"));
-    n.ok = n.get_uid && n.init && n.destroy && n.allgather && n.allreduce;
+    n.async_err = reinterpret_cast<nccl_async_err_fn>(dlsym(h, "ncclCommGetAsyncError"));
+    n.count = reinterpret_cast<nccl_count_fn>(dlsym(h, "ncclCommCount"));
+    n.abort = reinterpret_cast<nccl_abort_fn>(dlsym(h, "ncclCommAbort"));
+    n.ok = n.get_uid && n.init && n.destroy && n.allgather && n.allreduce && n.async_err && n.count && n.abort;
     if (!n.ok) snprintf(n.why, sizeof(n.why), "libnccl.so.2 lacks a required symbol");
   });
   return n;
@@ -820,7 +833,45 @@ mom_status_t nccl_fail(int rc, const char *what) {
   Nccl &n = nccl();
   return fail(MOM_ERR_NCCL, "%s: nccl error %d (%s)", what, rc, n.errstr ? n.errstr(rc) : "?");
 }
+// The communicator's asynchronous state (ncclCommGetAsyncError): a failed or aborted peer, a network or
+// CUDA error inside an earlier collective.  ncclSuccess (0) and ncclInProgress (7) are healthy.
+mom_status_t nccl_async_check(void *comm, const char *what) {
+  Nccl &n = nccl();
+  int st = 0;
+  int rc = n.async_err(comm, &st);
+  if (rc != 0) return nccl_fail(rc, "ncclCommGetAsyncError");
+  if (st != 0 && st != 7) return nccl_fail(st, what);
+  return MOM_OK;
+}
 }  // namespace
+
+mom_status_t mom_nccl_check(void *comm) {
+  g_err[0] = 0;
+  if (!comm) return fail(MOM_ERR_INVALID_ARG, "mom_nccl_check: null comm");
+  Nccl &n = nccl();
+  if (!n.ok) return fail(MOM_ERR_NCCL, "%s", n.why);
+  return nccl_async_check(comm, "communicator in error state");
+}
+
+mom_status_t mom_nccl_comm_count(void *comm, int *nranks_out) {
+  g_err[0] = 0;
+  if (!comm || !nranks_out) return fail(MOM_ERR_INVALID_ARG, "mom_nccl_comm_count: null pointer");
+  Nccl &n = nccl();
+  if (!n.ok) return fail(MOM_ERR_NCCL, "%s", n.why);
+  int rc = n.count(comm, nranks_out);
+  if (rc != 0) return nccl_fail(rc, "ncclCommCount");
+  return MOM_OK;
+}
+
+mom_status_t mom_nccl_comm_abort(void *comm) {
+  g_err[0] = 0;
+  if (!comm) return fail(MOM_ERR_INVALID_ARG, "mom_nccl_comm_abort: null comm");
+  Nccl &n = nccl();
+  if (!n.ok) return fail(MOM_ERR_NCCL, "%s", n.why);
+  int rc = n.abort(comm);
+  if (rc != 0) return nccl_fail(rc, "ncclCommAbort");
+  return MOM_OK;
+}
 
 mom_status_t mom_nccl_get_unique_id(void *id_out) {
   g_err[0] = 0;
@@ -872,7 +923,7 @@ mom_status_t mom_allgather_rows(void *rows, int64_t rows_per_rank, int64_t hidde
   const void *send = static_cast<const char *>(rows) + static_cast<size_t>(rank) * count * w;  // in-place
   int rc = n.allgather(send, rows, count, nccl_dtype, comm, static_cast<cudaStream_t>(stream));
   if (rc != 0) return nccl_fail(rc, "ncclAllGather");
-  return MOM_OK;
+  return nccl_async_check(comm, "ncclAllGather (async)");
 }
 
 mom_status_t mom_nccl_barrier(void *comm, int32_t *scratch, mom_stream_t stream) {
@@ -884,7 +935,7 @@ mom_status_t mom_nccl_barrier(void *comm, int32_t *scratch, mom_stream_t stream)
   // work on its stream (e.g. the peer stores of mom_mlp_minseq_fwd_gather) has completed
   int rc = n.allreduce(scratch, scratch, 1, 2 /* ncclInt32 */, 0 /* ncclSum */, comm, static_cast<cudaStream_t>(stream));
   if (rc != 0) return nccl_fail(rc, "ncclAllReduce(barrier)");
-  return MOM_OK;
+  return nccl_async_check(comm, "ncclAllReduce(barrier) (async)");
 }
 
 mom_status_t mom_argmax_allreduce(uint64_t *best_key, int32_t *argmax, void *comm, mom_stream_t stream) {
@@ -899,6 +950,8 @@ mom_status_t mom_argmax_allreduce(uint64_t *best_key, int32_t *argmax, void *com
     // u64 max over ranks of (order-preserving value << 32 | ~index): max logit, lowest index on ties
     int rc = n.allreduce(best_key, best_key, 1, 5 /* ncclUint64 */, 2 /* ncclMax */, comm, s);
     if (rc != 0) return nccl_fail(rc, "ncclAllReduce(max)");
+    mom_status_t st = nccl_async_check(comm, "ncclAllReduce(max) (async)");
+    if (st != MOM_OK) return st;
   }
   cudaError_t e = mom::launch_key_to_index(reinterpret_cast<const unsigned long long *>(best_key), argmax, s);
   if (e != cudaSuccess) return cuda_fail(e, "key to index");

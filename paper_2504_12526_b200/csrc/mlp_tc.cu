@@ -674,6 +674,20 @@ static cudaError_t launch(const Maps &maps, const Params &p, int num_sms, bool p
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 2 : 1;
+  if (MODE == MODE_FUSED) {
+    // phase-B tiles spin on counters released by phase-A tiles of OTHER clusters: every launched
+    // cluster must be co-resident (MPS / green-context SM limits, cluster placement), so clamp the
+    // grid to what can be active at once.  Tiles are taken in global order with a stride of the
+    // cluster count, so any resident cluster count makes progress.
+    int max_active = 0;
+    e = cudaOccupancyMaxActiveClusters(&max_active, kfn, &cfg);
+    if (e != cudaSuccess) return e;
+    if (max_active < 1) return cudaErrorLaunchOutOfResources;
+    if (clusters > static_cast<uint32_t>(max_active)) {
+      clusters = static_cast<uint32_t>(max_active);
+      cfg.gridDim = dim3(clusters * CG, 1, 1);
+    }
+  }
   return cudaLaunchKernelEx(&cfg, kfn, maps, p);
 }
 

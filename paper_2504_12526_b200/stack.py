@@ -129,9 +129,17 @@ class PrefillStack:
         """Exchange the cudaIpc handles of both gathered buffers and map every peer's, offset to this
         rank's shard rows (where this rank's phase-B epilogue stores its output rows)."""
         import torch.distributed as dist
-        mine = [_mom.ipc_get_handle(b) for b in self.xbuf]
+        try:
+            mine = [_mom.ipc_get_handle(b) for b in self.xbuf]
+            err = None
+        except _mom.MomError as e:  # every rank must still reach the all_gather below
+            mine, err = None, e
         handles = [None] * self.world
         dist.all_gather_object(handles, mine, group=self.group)
+        if err is not None:
+            raise err
+        if any(h is None for h in handles):
+            raise RuntimeError("a peer could not export its gathered buffers (cudaIpcGetMemHandle)")
         shard_off = self.rank * self.S * self.d * self.xbuf[0].element_size()
         for b in range(2):
             for r in range(self.world):
@@ -142,12 +150,14 @@ class PrefillStack:
                 self._peer_maps.append((ptr, off))
                 self.peers[b].append(ptr + shard_off)
 
-    def close(self):
-        """Unmap the peers' buffers (collective: every rank calls it after its last run)."""
+    def close(self, barrier: bool = True):
+        """Unmap the peers' buffers (collective: every rank calls it after its last run; barrier=False
+        only when no run was issued, e.g. after a failed setup)."""
         if self._peer_maps:
             import torch.distributed as dist
             torch.cuda.synchronize(self.device)
-            dist.barrier(group=self.group)  # no peer still stores into our buffers
+            if barrier:
+                dist.barrier(group=self.group)  # no peer still stores into our buffers
             for ptr, off in self._peer_maps:
                 _mom.ipc_close(ptr, off)
             self._peer_maps, self.peers = [], [[], []]

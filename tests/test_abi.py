@@ -175,3 +175,38 @@ def test_binding_checks_shapes():
         _mom.mlp_last_token(x[0], x[0], wg, wu, wd, torch.zeros(d + 8, dtype=bf))
     with pytest.raises(ValueError):
         _mom.lm_head_last(x[0], None, 1e-5, torch.zeros(40, d, dtype=bf), torch.zeros(41), torch.zeros(1, dtype=torch.int32))
+
+
+def test_binding_checks_copy_and_collective_sizes():
+    """the remaining entries check their buffer sizes in the binding (no out-of-bounds copy)."""
+    import torch
+    bf = torch.bfloat16
+    dev, host = torch.zeros(64, dtype=bf), torch.zeros(32, dtype=bf)
+    with pytest.raises(ValueError):
+        _mom.kv_offload(dev, host)               # host mirror smaller than the device K/V
+    with pytest.raises(ValueError):
+        _mom.kv_reload(host, dev)
+    with pytest.raises(ValueError):
+        _mom.kv_offload(dev, torch.zeros(64, dtype=bf), nbytes=129)  # more than either buffer
+    with pytest.raises(ValueError):               # logits shard shorter than the weight shard
+        _mom.lm_head_shard(torch.zeros(16, dtype=bf), None, 0.0, torch.zeros(40, 16, dtype=bf), 0,
+                           torch.zeros(39), torch.zeros(1, dtype=torch.int64))
+    with pytest.raises(ValueError):               # fewer rows than nranks * rows_per_rank
+        _mom.allgather_rows(torch.zeros(7, 16, dtype=bf), 4, 1, 0, 2)
+    S, d, I = 8, 16, 24
+    with pytest.raises(ValueError):               # folded-norm entry: W_down transposed
+        _mom.mlp_minseq_rmsnorm_fwd(torch.zeros(S, d, dtype=bf), torch.zeros(I, d, dtype=bf),
+                                    torch.zeros(I, d, dtype=bf), torch.zeros(I, d, dtype=bf),
+                                    torch.zeros(S, d, dtype=bf), 4, 1e-5)
+
+
+def test_nccl_failure_entries_reject_bad_arguments(lib):
+    """SURVEY §5 failure detection: the poll / count / abort entries validate before touching NCCL."""
+    E = _mom.MOM_ERR_INVALID_ARG
+    assert lib.mom_nccl_check(None) == E
+    assert lib.mom_nccl_comm_count(None, ctypes.byref(ctypes.c_int(0))) == E
+    assert lib.mom_nccl_comm_count(16, None) == E
+    assert lib.mom_nccl_comm_abort(None) == E
+    with pytest.raises(_mom.MomError) as ei:
+        _mom.nccl_check(None)
+    assert ei.value.status == E

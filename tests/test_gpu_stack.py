@@ -5,6 +5,8 @@ layer's last-token MLP, the LM head and the argmax are checked on the GPU's own 
 must match the stand-in bytewise on sampled rows, and the reload must match the host copy."""
 from __future__ import annotations
 
+import os
+
 import pytest
 import torch
 
@@ -102,10 +104,34 @@ def test_nccl_allgather_single_rank(cuda_device):
     comm = _mom.nccl_comm_init(1, uid, 0)
     rows = synth.hidden(128, 256, cuda_device, torch.bfloat16)
     ref = rows.clone()
+    assert _mom.nccl_comm_count(comm) == 1
     _mom.allgather_rows(rows, 128, comm, 0, 1)
     torch.cuda.synchronize()
+    _mom.nccl_check(comm)  # healthy communicator after the collective
     _mom.nccl_comm_destroy(comm)
     assert torch.equal(rows, ref)
+
+
+def test_ipc_export_failure_is_reported(cuda_device):
+    """Under torch's expandable_segments allocator (cuMemCreate memory) cudaIpcGetMemHandle fails: the
+    library must say so (MOM_ERR_CUDA with the reason) so callers fall back to the NCCL gather."""
+    import subprocess
+    import sys
+    code = ("import torch\n"
+            "from paper_2504_12526_b200 import _mom\n"
+            "t = torch.zeros(1 << 20, device='cuda')\n"
+            "try:\n"
+            "    _mom.ipc_get_handle(t)\n"
+            "    print('EXPORTED')\n"
+            "except _mom.MomError as e:\n"
+            "    print('STATUS', e.status, str(e))\n")
+    env = dict(os.environ, PYTORCH_CUDA_ALLOC_CONF="expandable_segments:True")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    out = r.stdout.strip()
+    assert r.returncode == 0, r.stderr[-2000:]
+    # either the driver exports it (then the fused path works) or the failure names the fallback
+    assert out == "EXPORTED" or (out.startswith(f"STATUS {_mom.MOM_ERR_CUDA}") and "NCCL" in out), out
 
 
 @pytest.mark.parametrize("nshards", [2, 3, 8])
