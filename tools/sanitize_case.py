@@ -1,5 +1,6 @@
 """Small tcgen05 MLP calls for compute-sanitizer: ragged mini-sequences with phase-A half-width tail
-tiles (S=2000, C=600, I=4096), both CTA-group modes, plus the last-token GEMVs and the LM head."""
+tiles (S=2000, C=600, I=4096), both CTA-group modes, the fused single-launch mode, the f1 gather into
+two local peer buffers, plus the last-token GEMVs and the LM head."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -16,6 +17,19 @@ for cg in ("2", "1"):
     out = torch.empty_like(x)
     _mom.mlp_minseq_fwd(x, x, wg, wu, wd, out, C)
     torch.cuda.synchronize()
+# fused single-launch mode (phase-B producers acquire phase-A row-block counters)
+os.environ["MOM_CTA_GROUP"] = "2"
+os.environ["MOM_FUSED"] = "1"
+out_f = torch.empty_like(x)
+_mom.mlp_minseq_fwd(x, x, wg, wu, wd, out_f, C)
+torch.cuda.synchronize()
+os.environ["MOM_FUSED"] = "0"
+# f1 gather: rank 1 of 3 with two local "peer" buffers (forwarding warps + epilogue peer stores)
+peers = [torch.zeros(3 * S, d, dtype=bf, device=dev) for _ in range(2)]
+mine = torch.zeros(3 * S, d, dtype=bf, device=dev)
+_mom.mlp_minseq_fwd_gather(x, x, wg, wu, wd, mine[S:2 * S], [p[S:2 * S] for p in peers], C)
+torch.cuda.synchronize()
+assert torch.equal(out_f, out) and all(torch.equal(p[S:2 * S], out) for p in peers + [mine])
 y = torch.empty(d, dtype=bf, device=dev)
 _mom.mlp_last_token(out[-1], out[-1], wg, wu, wd, y)
 wh = synth.head_weight(1000, d, dev, bf)
