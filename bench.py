@@ -72,6 +72,9 @@ def parse_args():
     ap.add_argument("--stack", action="store_true",
                     help="whole layer stack (PrefillStack) of --config (default config 5: Llama-3-8B, 32 layers, "
                          "S = 455000 tokens), token-sharded over the N ranks: strong scaling")
+    ap.add_argument("--early-reload", default="auto",
+                    help="--stack: f4 early KV reload budget ('auto' = all K/V minus the prefill transient, "
+                         "'off' = Alg. 1's order, or bytes); the other schedule is timed beside it")
     ap.add_argument("--layers", type=int, default=0,
                     help="--stack: run only this many layers (test mode; the line says so)")
     args = ap.parse_args()
@@ -241,7 +244,7 @@ class Workload:
         self.out = torch.empty((world * S, d), dtype=bf, device=device)  # gathered rows when world > 1
         from paper_2504_12526_b200 import _mom
         self.ws = torch.empty(_mom.mlp_minseq_workspace_bytes(S, d, I, C, bf), dtype=torch.uint8, device=device)
-        self.ws_last = torch.empty(_mom.lib().mom_mlp_last_token_workspace_bytes(I), dtype=torch.uint8, device=device)
+        self.ws_last = torch.empty(_mom.lib().mom_mlp_last_token_workspace_bytes(d, I), dtype=torch.uint8, device=device)
         self.ws_head = torch.empty(_mom.lib().mom_lm_head_workspace_bytes(V), dtype=torch.uint8, device=device)
         self.y = torch.empty(d, dtype=bf, device=device)
         self.logits = torch.empty(V, dtype=torch.float32, device=device)
@@ -852,7 +855,8 @@ def run_stack(args):
         box = []
         why = try_collective(lambda: box.append(PrefillStack(weights, wh, gain, cfg.eps, per, C, kv_shape, device,
                                                              world=world, rank=rank, comm=comm, S_total=S_total,
-                                                             gather="fused")), world, device)
+                                                             gather="fused", early_reload=args.early_reload)),
+                             world, device)
         if why is None:
             st = box[0]
         else:
@@ -863,7 +867,7 @@ def run_stack(args):
             gather, dist_info["gather_fallback_reason"] = "nccl", why
     if st is None:
         st = PrefillStack(weights, wh, gain, cfg.eps, per, C, kv_shape, device, world=world, rank=rank, comm=comm,
-                          S_total=S_total, gather=gather)
+                          S_total=S_total, gather=gather, early_reload=args.early_reload)
     x_work = torch.empty_like(x_mine) if world == 1 else None
     compute, copy = torch.cuda.Stream(device), torch.cuda.Stream(device)
 
@@ -905,6 +909,14 @@ def run_stack(args):
 
     with ClockSampler(device.index) as clk:
         ms, n_launch, res = timed(args.steps)
+    early_bytes = res.early_reload_bytes
+    # the other reload schedule, same run: Alg. 1's order (all reloads after the head) or early
+    budget, alt = st.early_budget, None
+    st.early_budget = 0 if budget > 0 else max(0, st.L * st.kv_bytes - st.transient_bytes)
+    if st.early_budget != budget:
+        a_ms, _, _ = timed(args.steps)
+        alt = {"early_reload_gb": st.early_budget / 1e9, "ms_per_step": a_ms, "value": S_total / (a_ms * 1e-3)}
+    st.early_budget = budget
     flops = 6.0 * S_total * d * I * (L - 1)
     ok, n_rows = verify_gathered_rows(st, x_full, weights, res.x_final)
     ok_all = bool(sum_over_ranks(1.0 if ok else 0.0, world, device) == world)
@@ -931,6 +943,10 @@ def run_stack(args):
                 "fraction divides the mini-sequence MLP FLOPs by the whole step time",
         "gpu_launches": int(sum_over_ranks(n_launch, world, device)),
         "gather_verified": ok_all, "gather_verified_rows_per_rank": n_rows,
+        "kv_reload": {"schedule": "early (f4: H2D of layer j after its D2H, within the device budget)" if budget
+                      else "Alg. 1 order (all after the head)", "early_reload_gb_per_rank": early_bytes / 1e9,
+                      "device_budget_gb": budget / 1e9, "prefill_transient_gb": st.transient_bytes / 1e9,
+                      "other_schedule": alt},
         "clocks": clk.summary(),
         "shared_gpu_test_mode": SHARED_GPU or None,
     }

@@ -289,12 +289,15 @@ __global__ void __launch_bounds__(THREADS, 2) last_token_splitk(const void *__re
   const size_t pitch_d = static_cast<size_t>(I) * 2;
   const char *wdb = static_cast<const char *>(wd) + static_cast<size_t>(j0) * 2 + v * 16;
   float *pb = partial + static_cast<size_t>(blockIdx.x) * d;
+  const size_t stride = pitch_d * (WARPS * 4);  // bytes between a lane's consecutive rows
   for (int c0 = wid * 4 + sub; c0 < d; c0 += WARPS * 4 * UD) {
     uint4 buf[UD];
+    const char *p = wdb + static_cast<size_t>(c0) * pitch_d;
 #pragma unroll
     for (int u = 0; u < UD; ++u) {
       const int c = c0 + u * WARPS * 4;
-      buf[u] = (active && c < d) ? ld_stream(wdb + c * pitch_d) : make_uint4(0u, 0u, 0u, 0u);
+      buf[u] = (active && c < d) ? ld_stream(p) : make_uint4(0u, 0u, 0u, 0u);
+      p += stride;
     }
 #pragma unroll
     for (int u = 0; u < UD; ++u) {
@@ -495,8 +498,8 @@ cudaError_t launch_last_token_mlp(const void *x, const void *residual, const voi
     const int nchunks = (I + SPLITK_J - 1) / SPLITK_J;
     const size_t smem = static_cast<size_t>(d) * sizeof(float);
     cudaError_t e;
-    if ((e = set_smem(last_token_splitk<16>, smem)) != cudaSuccess) return e;
-    last_token_splitk<16><<<nchunks, THREADS, smem, stream>>>(x, wg, wu, wd, h_ws, d, I);
+    if ((e = set_smem(last_token_splitk<12>, smem)) != cudaSuccess) return e;
+    last_token_splitk<12><<<nchunks, THREADS, smem, stream>>>(x, wg, wu, wd, h_ws, d, I);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((d + 63) / 64, 1, 1);

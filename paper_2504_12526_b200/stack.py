@@ -17,8 +17,13 @@ Pure control flow around the C-ABI calls (no arithmetic of the method runs here)
   4. final layer: mom_mlp_last_token on the last token, mom_lm_head_last on
      the rank that owns token S_total - 1;
   5. after the head, mom_kv_reload brings every layer's K/V back to the device, one
-     event per layer (f4: a decode step may start layer l as soon as its K/V is back; see
-     decode_consumer_pass).
+     event per layer (f4: a decode step may start layer l as soon as its K/V is back).
+     early_reload (f4, off by default = Alg. 1's order): the H2D of layer j may start as soon as its
+     D2H finished, on its own stream (PCIe is full duplex, so it runs beside the next layers'
+     offloads and MLPs), for as many layers as a device budget allows.  "auto" budget = all layers'
+     K/V minus the prefill transient (x, workspace, K/V ring): the device then never holds more than
+     at the end of Alg. 1 (weights + every layer's K/V), the paper's peak, while most of the
+     reload leaves the time to first token.  The rest is reloaded after the head, as in Alg. 1.
 Token sharding: rank r owns rows [r*S_r, (r+1)*S_r) of N*S_r (padded) rows.
 """
 from __future__ import annotations
@@ -65,6 +70,7 @@ class StackResult:
     # the final layer's input rows (all N*S_r rows when token-sharded; x itself on one GPU)
     x_final: torch.Tensor | None = None
     copy_stream: torch.cuda.Stream | None = None
+    early_reload_bytes: int = 0  # f4: bytes reloaded before the head (within the device budget)
 
 
 class PrefillStack:
@@ -78,7 +84,7 @@ class PrefillStack:
 
     def __init__(self, weights, w_head, norm_gain, eps, S_local, minseq_len, kv_shape, device,
                  world=1, rank=0, comm=None, S_total=None, offload=True, reload=True, gather="fused",
-                 group=None, pipelined_reload=False):
+                 group=None, pipelined_reload=False, early_reload="off"):
         self.weights = weights            # list of (w_gate, w_up, w_down), layer 0..L-1
         self.L = len(weights)
         self.wh, self.gain, self.eps = w_head, norm_gain, eps
@@ -99,7 +105,7 @@ class PrefillStack:
         self.V = w_head.shape[0]
         self.ws = torch.empty(_mom.mlp_minseq_workspace_bytes(S_local, self.d, self.I, minseq_len, self.dtype),
                               dtype=torch.uint8, device=device)
-        self.ws_last = torch.empty(_mom.lib().mom_mlp_last_token_workspace_bytes(self.I), dtype=torch.uint8,
+        self.ws_last = torch.empty(_mom.lib().mom_mlp_last_token_workspace_bytes(self.d, self.I), dtype=torch.uint8,
                                    device=device)
         self.ws_head = torch.empty(_mom.lib().mom_lm_head_workspace_bytes(self.V), dtype=torch.uint8, device=device)
         self.offload, self.reload = offload, reload and offload
@@ -114,6 +120,17 @@ class PrefillStack:
         self.logits = torch.empty(self.V, dtype=torch.float32, device=device)
         self.argmax = torch.empty(1, dtype=torch.int32, device=device)
         self.owner = last_token_owner(self.S_total, world)
+        self.kv_bytes = math.prod(kv_shape) * torch.empty((), dtype=self.dtype).element_size()
+        # device bytes prefill needs beyond the weights that are not part of Alg. 1's end state
+        x_bytes = (2 * world if world > 1 else 1) * S_local * self.d * torch.empty((), dtype=self.dtype).element_size()
+        self.transient_bytes = self.ws.numel() + len(self.kv_ring) * self.kv_bytes + x_bytes
+        if early_reload == "off" or not self.reload:
+            self.early_budget = 0
+        elif early_reload == "auto":
+            self.early_budget = max(0, self.L * self.kv_bytes - self.transient_bytes)
+        else:
+            self.early_budget = int(early_reload)
+        self.h2d = torch.cuda.Stream(device) if self.reload else None
         # the previous run's copies (offload into kv_host, reload out of it) must finish before a new
         # run refills the ring and the host mirrors (pipelined_reload leaves them in flight)
         self._prev_copies_done = None
@@ -184,10 +201,22 @@ class PrefillStack:
         compute = compute or torch.cuda.current_stream(self.device)
         copy = copy or torch.cuda.Stream(self.device)
         ev_off = [torch.cuda.Event() for _ in range(self.L)]
+        reload_done = []
+        reloaded = 0
+        h2d = self.h2d
+
+        def reload_layer(j):  # a10 for layer j on the H2D stream, after its D2H completed
+            ev = torch.cuda.Event()
+            h2d.wait_event(ev_off[j])
+            _mom.kv_reload(self.kv_host[j], self.kv_dev[j], h2d, ev)
+            reload_done.append(ev)
+
         launches = 0
         with torch.cuda.stream(compute):
             if self._prev_copies_done is not None:
                 compute.wait_event(self._prev_copies_done)
+                if h2d is not None:
+                    h2d.wait_event(self._prev_copies_done)
             if self.world > 1:
                 own = self.shard_of(self.xbuf[0])
                 src = x if x.shape[0] == self.S else self.shard_of(x)
@@ -201,6 +230,11 @@ class PrefillStack:
                     if kv_fill is not None:
                         kv_fill(l, slot)
                     _mom.kv_offload(slot, self.kv_host[l], compute, copy, ev_off[l])          # a9
+                    # f4 early reload of the layers already offloaded, within the device budget
+                    while (self.reload and len(reload_done) <= l and
+                           reloaded + self.kv_bytes <= self.early_budget):
+                        reload_layer(len(reload_done))
+                        reloaded += self.kv_bytes
                 cur = x if self.world == 1 else self.xbuf[gathered_buffer_index(l)]
                 if on_layer is not None:
                     on_layer(l, cur)
@@ -227,13 +261,11 @@ class PrefillStack:
                                       self.ws_head, compute)                                       # a7-a8
                     launches += 4
             x_final = x if self.world == 1 else self.xbuf[gathered_buffer_index(self.L - 1)]
-            reload_done = []
             if self.reload:
-                copy.wait_stream(compute)  # Alg. 1: after the head
-                for l in range(self.L):     # layer order = decode order (f4: per-layer completion)
-                    ev = torch.cuda.Event()
-                    _mom.kv_reload(self.kv_host[l], self.kv_dev[l], copy, ev)                      # a10
-                    reload_done.append(ev)
+                h2d.wait_stream(compute)   # Alg. 1: the rest after the head
+                for j in range(len(reload_done), self.L):  # layer order = decode order (f4)
+                    reload_layer(j)
+                copy.wait_stream(h2d)
             done = torch.cuda.Event()
             done.record(copy)
             self._prev_copies_done = done
@@ -241,4 +273,4 @@ class PrefillStack:
                 compute.wait_stream(copy)
         own = self.rank == self.owner
         return StackResult(self.y if own else None, self.logits if own else None, self.argmax if own else None,
-                           self.kv_host, self.kv_dev, launches, reload_done, x_final, copy)
+                           self.kv_host, self.kv_dev, launches, reload_done, x_final, copy, reloaded)

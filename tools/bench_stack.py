@@ -1,6 +1,8 @@
 #!/usr/bin/env python
 """Measure the full MOM prefill MLP path over a model's layer stack (BASELINE configs 3, 4, 5 at N=1).
 
+Modes: no_offload, offload_no_reload, full (Alg. 1: reload after the head), full_early (f4: the
+reload of layer j starts after its offload, within the device budget; the rest after the head).
 One step = Alg. 1 over all L layers (paper_2504_12526_b200.stack.PrefillStack): per layer the K/V
 stand-in is offloaded on the copy stream while the mini-sequence MLP runs (L-1 layers), the final
 layer runs on the last token, then LM head + argmax, then every layer's K/V is reloaded.  Also timed:
@@ -50,9 +52,10 @@ def main():
     peaks, src = load_peaks()
     out = {"workload": w.name, "hidden": d, "intermediate": I, "vocab": V, "layers": L, "S": S, "minseq_len": C,
            "M": -(-S // C), "kv_bytes_per_layer": S * 2 * w.d_kv * 2}
-    for mode in ("no_offload", "offload_no_reload", "full"):
+    for mode in ("no_offload", "offload_no_reload", "full", "full_early"):
         st = PrefillStack(weights, wh, gain, w.eps, S, C, (S, 2 * w.d_kv), dev,
-                          offload=mode != "no_offload", reload=mode == "full")
+                          offload=mode != "no_offload", reload=mode.startswith("full"),
+                          early_reload="auto" if mode == "full_early" else "off")
         for _ in range(args.warmup):
             x.copy_(x0)
             st.run(x, kv_fill, compute, copy)
@@ -77,6 +80,9 @@ def main():
                      "mlp_tflops": flops / (mlp_ms * 1e-3) / 1e12,
                      "mlp_frac_sustained": flops / (mlp_ms * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"],
                      "clocks": clk.summary()}
+        if mode == "full_early":
+            out[mode]["early_reload_gb"] = st.early_budget // st.kv_bytes * st.kv_bytes / 1e9
+            out[mode]["prefill_transient_gb"] = st.transient_bytes / 1e9
         if "lm_head_gemv" in per:
             t = statistics.mean(per["lm_head_gemv"])
             out[mode]["lm_head_ms"] = t
@@ -95,6 +101,7 @@ def main():
         torch.cuda.empty_cache()
     out["offload_overlap_ratio"] = out["offload_no_reload"]["ms_per_step"] / out["no_offload"]["ms_per_step"]
     out["reload_ms"] = out["full"]["ms_per_step"] - out["offload_no_reload"]["ms_per_step"]
+    out["reload_ms_early"] = out["full_early"]["ms_per_step"] - out["offload_no_reload"]["ms_per_step"]
     out["peak_source"] = src
     print(json.dumps(out), flush=True)
 
