@@ -244,7 +244,7 @@ class Workload:
         self.out = torch.empty((world * S, d), dtype=bf, device=device)  # gathered rows when world > 1
         from paper_2504_12526_b200 import _mom
         self.ws = torch.empty(_mom.mlp_minseq_workspace_bytes(S, d, I, C, bf), dtype=torch.uint8, device=device)
-        self.ws_last = torch.empty(_mom.lib().mom_mlp_last_token_workspace_bytes(d, I), dtype=torch.uint8, device=device)
+        self.ws_last = torch.empty(_mom.lib().mom_mlp_last_token_workspace_bytes(I), dtype=torch.uint8, device=device)
         self.ws_head = torch.empty(_mom.lib().mom_lm_head_workspace_bytes(V), dtype=torch.uint8, device=device)
         self.y = torch.empty(d, dtype=bf, device=device)
         self.logits = torch.empty(V, dtype=torch.float32, device=device)

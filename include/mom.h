@@ -160,16 +160,12 @@ mom_status_t mom_mlp_minseq_rmsnorm_fwd(const void *x, const void *w_gate_folded
 /* ------------------------------------------------------------------------------------
  * a6. Final layer on the last token only.  Alg. 1: A_last = A[:, -1, :]
  * (pass x + (S-1)*hidden), O_last = MLP(A_last) (+ residual_last if non-NULL).
- * HBM-bound: h = Swish(W_gate x) (.) (W_up x) in fp32, out_last = residual_last + W_down h
- * rounded once to dt.  bf16: one streaming launch, split-K over 64-wide chunks of the intermediate
- * dimension (each block computes its 64 h values and their W_down columns' contribution to every
- * output; chunk partials (fp32, in `workspace`) summed in chunk order by a second, PDL-chained
- * kernel).  fp32: the GEMV pair (h in `workspace`, then W_down h).
+ * HBM-bound GEMV pair: h = Swish(W_gate x) (.) (W_up x) kept in fp32 in `workspace`, then
+ * out_last = residual_last + W_down h rounded once to dt.
  *   x_last, residual_last (or NULL), out_last: device [hidden]; weights as above.
- *   workspace >= mom_mlp_last_token_workspace_bytes(hidden, intermediate)
- *              = max(intermediate, ceil(intermediate / 64) * hidden) * 4 bytes, rounded to 256.
+ *   workspace >= mom_mlp_last_token_workspace_bytes(intermediate).
  * ---------------------------------------------------------------------------------- */
-size_t mom_mlp_last_token_workspace_bytes(int64_t hidden, int64_t intermediate);
+size_t mom_mlp_last_token_workspace_bytes(int64_t intermediate);
 mom_status_t mom_mlp_last_token(const void *x_last, const void *residual_last, const void *w_gate,
                                 const void *w_up, const void *w_down, void *out_last,
                                 int64_t hidden, int64_t intermediate, mom_dtype_t dt,

@@ -30,7 +30,7 @@ SIGNATURES = {
     "mom_fold_norm_gain": (_i32, [_p, _p, _p, _i64, _i64, _i32, _p]),
     "mom_mlp_minseq_rmsnorm_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64, _i32]),
     "mom_mlp_minseq_rmsnorm_fwd": (_i32, [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _f32, _i32, _p, _sz, _p]),
-    "mom_mlp_last_token_workspace_bytes": (_sz, [_i64, _i64]),
+    "mom_mlp_last_token_workspace_bytes": (_sz, [_i64]),
     "mom_mlp_last_token": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _p, _sz, _p]),
     "mom_lm_head_workspace_bytes": (_sz, [_i64]),
     "mom_lm_head_last": (_i32, [_p, _p, _f32, _p, _p, _p, _i64, _i64, _i32, _p, _sz, _p]),
@@ -281,7 +281,7 @@ def mlp_last_token(x_last, residual_last, w_gate, w_up, w_down, out_last, worksp
     I = w_gate.shape[0]
     dt = _dt(x_last)
     if workspace is None:
-        workspace = torch.empty(lib().mom_mlp_last_token_workspace_bytes(hidden, I), dtype=torch.uint8, device=x_last.device)
+        workspace = torch.empty(lib().mom_mlp_last_token_workspace_bytes(I), dtype=torch.uint8, device=x_last.device)
     _check(lib().mom_mlp_last_token(_ptr(x_last), _ptr(residual_last), _ptr(w_gate), _ptr(w_up), _ptr(w_down),
                                     _ptr(out_last), hidden, I, dt, _ptr(workspace),
                                     workspace.numel() * workspace.element_size(), _stream(stream)))

@@ -627,11 +627,9 @@ mom_status_t mom_mlp_minseq_rmsnorm_fwd(const void *x, const void *w_gate_folded
                     static_cast<cudaStream_t>(stream), nullptr, nullptr, &eps);
 }
 
-size_t mom_mlp_last_token_workspace_bytes(int64_t hidden, int64_t intermediate) {
-  if (hidden < 1 || intermediate < 1 || hidden > (1 << 24) || intermediate > (1 << 24)) return 0;
-  // fp32 h (two-launch pair) or the split-K chunk partials ceil(I/64) x hidden fp32, whichever is larger
-  return (mom::last_token_workspace(static_cast<int>(hidden), static_cast<int>(intermediate)) + 255) &
-         ~static_cast<size_t>(255);
+size_t mom_mlp_last_token_workspace_bytes(int64_t intermediate) {
+  if (intermediate < 1) return 0;
+  return ((static_cast<size_t>(intermediate) * 4) + 255) & ~static_cast<size_t>(255);  // h, fp32
 }
 
 mom_status_t mom_mlp_last_token(const void *x_last, const void *residual_last, const void *w_gate,
@@ -656,7 +654,7 @@ mom_status_t mom_mlp_last_token(const void *x_last, const void *residual_last, c
     return fail(MOM_ERR_INVALID_ARG, "mom_mlp_last_token: out_last may alias x_last only when residual_last does too");
   if (hidden > (1 << 24) || intermediate > (1 << 24))
     return fail(MOM_ERR_UNSUPPORTED, "mom_mlp_last_token: staging buffers limit hidden/intermediate to 2^24");
-  const size_t need = mom_mlp_last_token_workspace_bytes(hidden, intermediate);
+  const size_t need = mom_mlp_last_token_workspace_bytes(intermediate);
   if (workspace_bytes < need) return fail(MOM_ERR_WORKSPACE, "mom_mlp_last_token: workspace %zu < %zu", workspace_bytes, need);
   if (static_cast<size_t>(intermediate) * 4 > 227 * 1024 || static_cast<size_t>(hidden) * 4 > 227 * 1024)
     return fail(MOM_ERR_UNSUPPORTED, "mom_mlp_last_token: vector does not fit in shared memory");

@@ -1,8 +1,5 @@
 // gemv.cu -- HBM-streaming kernels of MOM's last-token path (Alg. 1):
 //   * last_token_mlp: O_last = residual + W_down (Swish(W_gate x) (.) W_up x)
-//       bf16 default (MOM_GEMV_VARIANT=2): last_token_splitk streams all 3*d*I*w bytes in one launch,
-//       split-K over 64-wide chunks of I, then last_token_reduce (PDL) sums the chunk partials.
-//       The two-launch pair (MOM_GEMV_VARIANT=1, and fp32):
 //       kernel 1 streams W_gate and W_up (2*I*d*w bytes), keeps h in fp32;
 //       kernel 2 streams W_down (d*I*w bytes), launched with PDL: it prefetches its W_down
 //       rows into L2 while kernel 1 runs, then waits (griddepcontrol) and reads h via L1.
@@ -241,90 +238,6 @@ __global__ void __launch_bounds__(THREADS, MINB) down_gemv(const float *__restri
   }
 }
 
-// ---- last-token MLP in ONE streaming launch: split-K over the intermediate dimension ----
-// Block b owns the chunk J_b = [64 b, 64 b + 64) of intermediate indices and streams everything that
-// chunk needs, with no dependency on any other block:
-//   h_j = Swish(W_gate[j] . x) * (W_up[j] . x)     j in J_b   (2 x 64 weight rows of d)
-//   p_b[c] = sum_{j in J_b} h_j W_down[c, j]        all c      (d row segments of 64 x 2 = 128 B)
-// and last_token_reduce adds out[c] = residual[c] + sum_b p_b[c] (b ascending, fixed order).  The
-// 3 d I w bytes stream in a single wave (ceil(I/64) <= 2 blocks per SM resident for I <= 18944 on 148
-// SMs) instead of two dependent launches, so there is one ramp-up and one tail, and W_down streams
-// while other blocks still read W_gate / W_up.  Partials: ceil(I/64) x d fp32 (3.7 MB at config 2,
-// L2-resident).
-constexpr int SPLITK_J = 64;
-
-template <int UD>
-__global__ void __launch_bounds__(THREADS, 2) last_token_splitk(const void *__restrict__ x, const void *__restrict__ wg,
-                                                             const void *__restrict__ wu, const void *__restrict__ wd,
-                                                             float *__restrict__ partial, int d, int I) {
-  extern __shared__ float xs[];
-  __shared__ float hs[SPLITK_J];
-  pdl_launch_dependents();  // the reduction kernel may launch now (it waits for this grid)
-  stage_vec<true>(x, xs, d);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int j0 = blockIdx.x * SPLITK_J;
-  const int nj = I - j0 < SPLITK_J ? I - j0 : SPLITK_J;
-  const size_t pitch = static_cast<size_t>(d) * 2;
-  // gate/up rows of the chunk: 4 row pairs per warp step (x read once per 8 rows)
-  for (int r0 = wid * 4; r0 < nj; r0 += WARPS * 4) {
-    float gu[2][4];
-    const char *const base[2] = {static_cast<const char *>(wg) + (j0 + r0) * pitch,
-                                 static_cast<const char *>(wu) + (j0 + r0) * pitch};
-    rows_dot<true, 2, 4, false, 2>(base, pitch, nj - r0, xs, d, lane, gu);
-    if (lane == 0) {
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (r0 + r < nj) hs[r0 + r] = gu[0][r] / (1.0f + __expf(-gu[0][r])) * gu[1][r];
-    }
-  }
-  __syncthreads();
-  // W_down[:, J_b]: lane = (row sub-index 0..3) x (16-B vector 0..7 of the 128-B segment); one warp
-  // instruction reads 4 full 128-B row segments; the 8 j-values of a lane stay in registers
-  const int v = lane & 7, sub = lane >> 3;
-  const bool active = 8 * v < nj;
-  float hv[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) hv[e] = active ? hs[8 * v + e] : 0.f;
-  const size_t pitch_d = static_cast<size_t>(I) * 2;
-  const char *wdb = static_cast<const char *>(wd) + static_cast<size_t>(j0) * 2 + v * 16;
-  float *pb = partial + static_cast<size_t>(blockIdx.x) * d;
-  const size_t stride = pitch_d * (WARPS * 4);  // bytes between a lane's consecutive rows
-  for (int c0 = wid * 4 + sub; c0 < d; c0 += WARPS * 4 * UD) {
-    uint4 buf[UD];
-    const char *p = wdb + static_cast<size_t>(c0) * pitch_d;
-#pragma unroll
-    for (int u = 0; u < UD; ++u) {
-      const int c = c0 + u * WARPS * 4;
-      buf[u] = (active && c < d) ? ld_stream(p) : make_uint4(0u, 0u, 0u, 0u);
-      p += stride;
-    }
-#pragma unroll
-    for (int u = 0; u < UD; ++u) {
-      float s = dot8_bf16(buf[u], hv);
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      s += __shfl_xor_sync(0xffffffffu, s, 4);
-      const int c = c0 + u * WARPS * 4;
-      if (v == 0 && c < d) pb[c] = s;
-    }
-  }
-}
-
-// out[c] = residual[c] + sum_b partial[b][c], b ascending (one rounding of the fp32 sum).
-__global__ void __launch_bounds__(64) last_token_reduce(const float *__restrict__ partial, int nchunks,
-                                                      const __nv_bfloat16 *__restrict__ residual,
-                                                      __nv_bfloat16 *__restrict__ out, int d) {
-  pdl_wait();  // every block of last_token_splitk has written its partials
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= d) return;
-  float s = 0.f;
-#pragma unroll 8
-  for (int b = 0; b < nchunks; ++b) s += partial[static_cast<size_t>(b) * d + c];
-  const float rv = residual ? __bfloat162float(residual[c]) : 0.f;
-  out[c] = __float2bfloat16_rn(rv + s);
-}
-
 // Order-preserving map float -> uint32 (larger float -> larger key), then pack with the
 // complemented index so that the u64 max picks the largest value and, among equal
 // values, the LOWEST index.
@@ -483,42 +396,15 @@ static cudaError_t last_token_pair(const void *x, const void *residual, const vo
   return cudaGetLastError();
 }
 
-size_t last_token_workspace(int d, int I) {
-  const size_t pair = static_cast<size_t>(I) * 4;  // h (fp32) of the two-launch pair
-  const size_t splitk = static_cast<size_t>((I + gemv::SPLITK_J - 1) / gemv::SPLITK_J) * d * 4;  // partials
-  return pair > splitk ? pair : splitk;
-}
-
 cudaError_t launch_last_token_mlp(const void *x, const void *residual, const void *wg, const void *wu,
                                   const void *wd, void *out, float *h_ws, int d, int I, bool is_bf16, int num_sms,
                                   cudaStream_t stream) {
-  const int variant = gemv::env_or("MOM_GEMV_VARIANT", 2);
-  if (is_bf16 && variant == 2) {
-    using namespace gemv;
-    const int nchunks = (I + SPLITK_J - 1) / SPLITK_J;
-    const size_t smem = static_cast<size_t>(d) * sizeof(float);
-    cudaError_t e;
-    if ((e = set_smem(last_token_splitk<12>, smem)) != cudaSuccess) return e;
-    last_token_splitk<12><<<nchunks, THREADS, smem, stream>>>(x, wg, wu, wd, h_ws, d, I);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((d + 63) / 64, 1, 1);
-    cfg.blockDim = dim3(64, 1, 1);
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = env_or("MOM_GEMV_PDL", 1) != 0;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, last_token_reduce, static_cast<const float *>(h_ws), nchunks,
-                              static_cast<const __nv_bfloat16 *>(residual), static_cast<__nv_bfloat16 *>(out), d);
-  }
   // (rows per warp step, 16-B loads in flight per row, min blocks per SM) for gate/up and down.
   // Down: 2 rows x 4 loads in flight at 2 blocks/SM (2048 warps, 16 MB in flight) instead of
   // 2 x 2 at 4/SM (4 MB in flight: latency-bound at ~3.5 TB/s); measured 74.8 -> 64.5-67.6 us
   // for the pair (profiles/r1_gemv_variants.txt).  MOM_GEMV_VARIANT=0 restores the old shape.
   if (!is_bf16) return last_token_pair<false, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
-  if (variant == 0)
+  if (gemv::env_or("MOM_GEMV_VARIANT", 1) == 0)
     return last_token_pair<true, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
   return last_token_pair<true, 2, 2, 4, 2, 4, 2>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
 }

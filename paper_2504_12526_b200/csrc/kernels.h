@@ -59,7 +59,6 @@ cudaError_t launch_phase_b_f32(const float *h, const float *wd, const float *res
                                int I, cudaStream_t stream);
 
 // GEMV path (gemv.cu).  is_bf16 selects bf16 vs fp32 storage of x/w/out.
-size_t last_token_workspace(int d, int I);  // bytes of h_ws for launch_last_token_mlp
 cudaError_t launch_last_token_mlp(const void *x, const void *residual, const void *wg, const void *wu,
                                   const void *wd, void *out, float *h_ws, int d, int I, bool is_bf16,
                                   int num_sms, cudaStream_t stream);

@@ -105,7 +105,7 @@ class PrefillStack:
         self.V = w_head.shape[0]
         self.ws = torch.empty(_mom.mlp_minseq_workspace_bytes(S_local, self.d, self.I, minseq_len, self.dtype),
                               dtype=torch.uint8, device=device)
-        self.ws_last = torch.empty(_mom.lib().mom_mlp_last_token_workspace_bytes(self.d, self.I), dtype=torch.uint8,
+        self.ws_last = torch.empty(_mom.lib().mom_mlp_last_token_workspace_bytes(self.I), dtype=torch.uint8,
                                    device=device)
         self.ws_head = torch.empty(_mom.lib().mom_lm_head_workspace_bytes(self.V), dtype=torch.uint8, device=device)
         self.offload, self.reload = offload, reload and offload

@@ -211,10 +211,3 @@ def test_nccl_failure_entries_reject_bad_arguments(lib):
         _mom.nccl_check(None)
     assert ei.value.status == E
 
-
-def test_last_token_workspace_covers_split_k_partials(lib):
-    """bf16 last token: ceil(I/64) chunk partials of `hidden` fp32 each (or I fp32 of h, if larger)."""
-    assert lib.mom_mlp_last_token_workspace_bytes(4096, 14336) == 224 * 4096 * 4
-    assert lib.mom_mlp_last_token_workspace_bytes(256, 688) == -(-11 * 256 * 4 // 256) * 256
-    assert lib.mom_mlp_last_token_workspace_bytes(8, 4096) == 4096 * 4  # h dominates
-    assert lib.mom_mlp_last_token_workspace_bytes(0, 4096) == 0
