@@ -84,7 +84,7 @@ class PrefillStack:
 
     def __init__(self, weights, w_head, norm_gain, eps, S_local, minseq_len, kv_shape, device,
                  world=1, rank=0, comm=None, S_total=None, offload=True, reload=True, gather="fused",
-                 group=None, pipelined_reload=False, early_reload="off"):
+                 group=None, pipelined_reload=False, early_reload="off", defer_last_offload=True):
         self.weights = weights            # list of (w_gate, w_up, w_down), layer 0..L-1
         self.L = len(weights)
         self.wh, self.gain, self.eps = w_head, norm_gain, eps
@@ -112,6 +112,7 @@ class PrefillStack:
         # f4: when True, run() does not join the copy stream after the reload; the caller waits
         # on StackResult.reload_done[l] per layer (decode of layer l overlaps the H2D of l+1..)
         self.pipelined_reload = pipelined_reload
+        self.defer_last_offload = defer_last_offload
         self.kv_shape = kv_shape
         self.kv_ring = [torch.empty(kv_shape, dtype=self.dtype, device=device) for _ in range(2)] if offload else []
         self.kv_host = [torch.empty(kv_shape, dtype=self.dtype, pin_memory=True) for _ in range(self.L)] if offload else []
@@ -222,6 +223,15 @@ class PrefillStack:
                 src = x if x.shape[0] == self.S else self.shard_of(x)
                 if src.data_ptr() != own.data_ptr():
                     own.copy_(src)
+            def offload_layer(l, slot):                                                        # a9
+                nonlocal reloaded
+                _mom.kv_offload(slot, self.kv_host[l], compute, copy, ev_off[l])
+                # f4 early reload of the layers already offloaded, within the device budget
+                while (self.reload and len(reload_done) <= l and
+                       reloaded + self.kv_bytes <= self.early_budget):
+                    reload_layer(len(reload_done))
+                    reloaded += self.kv_bytes
+
             for l in range(self.L):
                 if self.offload:
                     slot = self.kv_ring[l % 2]
@@ -229,12 +239,11 @@ class PrefillStack:
                         compute.wait_event(ev_off[l - 2])   # slot reuse only after its D2H finished
                     if kv_fill is not None:
                         kv_fill(l, slot)
-                    _mom.kv_offload(slot, self.kv_host[l], compute, copy, ev_off[l])          # a9
-                    # f4 early reload of the layers already offloaded, within the device budget
-                    while (self.reload and len(reload_done) <= l and
-                           reloaded + self.kv_bytes <= self.early_budget):
-                        reload_layer(len(reload_done))
-                        reloaded += self.kv_bytes
+                    # the final layer's D2H is issued after the head: its few hundred us of GEMVs
+                    # would otherwise share HBM with the copy engine (-20 % LM-head bandwidth,
+                    # profiles/r2_summary.md); the copy itself is the same
+                    if l < self.L - 1 or not self.defer_last_offload:
+                        offload_layer(l, slot)
                 cur = x if self.world == 1 else self.xbuf[gathered_buffer_index(l)]
                 if on_layer is not None:
                     on_layer(l, cur)
@@ -260,6 +269,8 @@ class PrefillStack:
                     _mom.lm_head_last(self.y, self.gain, self.eps, self.wh, self.logits, self.argmax,
                                       self.ws_head, compute)                                       # a7-a8
                     launches += 4
+            if self.offload and self.defer_last_offload:
+                offload_layer(self.L - 1, self.kv_ring[(self.L - 1) % 2])
             x_final = x if self.world == 1 else self.xbuf[gathered_buffer_index(self.L - 1)]
             if self.reload:
                 h2d.wait_stream(compute)   # Alg. 1: the rest after the head

@@ -49,7 +49,8 @@ def test_knobs_are_bit_neutral(cuda_device):
 
 
 GEMV_KNOBS = [{}, {"MOM_GEMV_VARIANT": "0"}, {"MOM_GEMV_PDL": "0"}, {"MOM_GEMV_PREFETCH": "2"},
-              {"MOM_GEMV_VARIANT": "0", "MOM_GEMV_PDL": "0"}]
+              {"MOM_GEMV_VARIANT": "0", "MOM_GEMV_PDL": "0"}, {"MOM_GEMV_VARIANT": "1"},
+              {"MOM_GEMV_VARIANT": "2"}, {"MOM_GEMV_VARIANT": "3"}]
 GEMV_ALL = sorted({k for v in GEMV_KNOBS for k in v})
 
 
