@@ -79,3 +79,31 @@ for G in (4, 8, 16):
 for GN in (2, 4, 8):
     print(f"col groups of {GN} (n fastest)        ", run(tiles_col_grouped(GN)))
     print(f"col groups of {GN} + K rev odd n      ", run(tiles_col_grouped(GN), lambda m, n: n % 2 == 1))
+
+
+def run_wave_rev(order, l2_mb=args.l2_mb):
+    """K reversed on every other WAVE (not C-invariant: a lower bound for K-direction tricks)."""
+    cap = int(l2_mb * 1024 * 1024 / SL)
+    lru = OrderedDict()
+    miss = {"A": 0, "B": 0, "epi": 0}
+    def touch(key, kind):
+        if key in lru:
+            lru.move_to_end(key); return
+        miss[kind] += 1; lru[key] = 1
+        while len(lru) > cap: lru.popitem(last=False)
+    waves = [order[i:i + clusters] for i in range(0, len(order), clusters)]
+    for wi, w in enumerate(waves):
+        for k in range(kb):
+            kk = kb - 1 - k if wi % 2 else k
+            for (m, n) in w:
+                touch(("A", m, kk), "A"); touch(("B", n, kk), "B")
+        for (m, n) in w:
+            for q in range(8): touch(("E", m, n, q), "epi")
+    return {k: round(v * SL / 1e9, 3) for k, v in miss.items()}
+
+
+print("--- lower bounds (wave-parity K reversal, not C-invariant)")
+for G in (4, 8, 16):
+    print(f"group_m={G:2d} wave-rev                ", run_wave_rev(tiles_grouped(G)))
+for GN in (4, 8):
+    print(f"col groups of {GN} wave-rev           ", run_wave_rev(tiles_col_grouped(GN)))
