@@ -757,7 +757,9 @@ def run_mine(args):
         e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, device)
         result["e2e"] = {"value": total_tokens / (e_ms / 1e3), "unit": "tokens/s",
                          "h2d_bytes_per_step": int(world * wl.x.numel() * 2),
-                         "d2h_bytes_per_step": int(wl.V * 4 + 4), "ms_per_step": e_ms}
+                         "d2h_bytes_per_step": int(wl.V * 4 + 4), "ms_per_step": e_ms,
+                         "result_read_back": "the last token's logits + greedy token (Alg. 1 returns L, P:107); "
+                                             "the [S, d] MLP output stays in HBM as the next layer's input"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(wl)

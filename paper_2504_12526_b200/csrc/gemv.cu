@@ -192,6 +192,9 @@ __global__ void __launch_bounds__(THREADS, MINB) gate_up_gemv(const void *__rest
                                                            const void *__restrict__ wu, float *__restrict__ h, int d,
                                                            int I) {
   pdl_launch_dependents();  // the down GEMV may launch now
+  // launched with PDL after the producer of x (the last mini-sequence layer's phase B): the CTAs
+  // become resident as that grid's CTAs retire, and wait here for its results
+  pdl_wait();
   extern __shared__ float xs[];
   stage_vec<BF16>(x, xs, d);
   __syncthreads();
@@ -385,11 +388,13 @@ static cudaError_t last_token_pair(const void *x, const void *residual, const vo
   };
   const int blocks1 = balanced_blocks((I + RG - 1) / RG, MG);
   const int blocks2 = balanced_blocks((d + RD - 1) / RD, MD);
-  const bool pdl = env_or("MOM_GEMV_PDL", 1) != 0;     // PDL launch of the down GEMV
+  const bool pdl = env_or("MOM_GEMV_PDL", 1) != 0;     // PDL launches of both GEMVs
   const int pf = env_or("MOM_GEMV_PREFETCH", 0);        // W_down rows per warp prefetched to L2 first
   cudaError_t e;
   if ((e = set_smem(gate_up_gemv<BF16, RG, UG, MG>, smem1)) != cudaSuccess) return e;
-  gate_up_gemv<BF16, RG, UG, MG><<<blocks1, THREADS, smem1, stream>>>(x, wg, wu, h_ws, d, I);
+  if ((e = launch_maybe_pdl(gate_up_gemv<BF16, RG, UG, MG>, blocks1, smem1, stream, pdl, x, wg, wu, h_ws, d, I)) !=
+      cudaSuccess)
+    return e;
   if ((e = launch_maybe_pdl(down_gemv<BF16, RD, UD, MD>, blocks2, 0, stream, pdl, h_ws, wd, residual, out, d, I, pf)) !=
       cudaSuccess)
     return e;
