@@ -175,14 +175,14 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
-// Prefetch (into L2) the weight rows this block's warps will stream: rows w, w + stride, ...
-__device__ __forceinline__ void prefetch_my_rows(const void *base, size_t pitch, int rows, int max_rows_per_warp) {
+// Prefetch (into L2) the first `bytes` of the R consecutive weight rows this warp streams first
+// (rows w*R .. w*R+R-1): issued before griddepcontrol.wait, so they arrive while the primary grid
+// drains and the warp's first loads hit L2.
+__device__ __forceinline__ void prefetch_first_rows(const void *base, size_t pitch, int rows, int R, uint32_t bytes) {
   const int lane = threadIdx.x & 31;
   const int w = blockIdx.x * WARPS + (threadIdx.x >> 5);
-  if (lane < max_rows_per_warp) {
-    const int r = w + lane * gridDim.x * WARPS;
-    if (r < rows) prefetch_l2_bulk(static_cast<const char *>(base) + r * pitch, static_cast<uint32_t>(pitch));
-  }
+  const int r = w * R + lane;
+  if (lane < R && r < rows) prefetch_l2_bulk(static_cast<const char *>(base) + r * pitch, bytes);
 }
 
 // h[j] = Swish(sum_k x_k Wg[j,k]) * (sum_k x_k Wu[j,k]), fp32.  Warp-stride over groups of R
@@ -217,12 +217,13 @@ __global__ void __launch_bounds__(THREADS, MINB) gate_up_gemv(const void *__rest
 template <bool BF16, int R, int U = 2, int MINB = 4>
 __global__ void __launch_bounds__(THREADS, MINB) down_gemv(const float *__restrict__ h, const void *__restrict__ wd,
                                                         const void *__restrict__ residual, void *__restrict__ out,
-                                                        int d, int I, int prefetch_rows) {
+                                                        int d, int I, int prefetch_bytes) {
   const int lane = threadIdx.x & 31;
   const int w = blockIdx.x * WARPS + (threadIdx.x >> 5);
   const size_t pitch = static_cast<size_t>(I) * (BF16 ? 2 : 4);
-  // W_down does not depend on h: optionally pull this warp's rows towards L2 while gate/up runs
-  if ((pitch & 15) == 0 && prefetch_rows > 0) prefetch_my_rows(wd, pitch, d, prefetch_rows);
+  // W_down does not depend on h: pull the head of this warp's first rows towards L2 while gate/up
+  // drains (prefetch_bytes per row, 16-B multiple, <= the row)
+  if (prefetch_bytes > 0) prefetch_first_rows(wd, pitch, d, R, static_cast<uint32_t>(prefetch_bytes));
   pdl_launch_dependents();  // the LM head may launch early too
   pdl_wait();               // h (written by gate_up_gemv) is complete and visible from here on
   for (int c0 = w * R; c0 < d; c0 += gridDim.x * WARPS * R) {
@@ -389,7 +390,11 @@ static cudaError_t last_token_pair(const void *x, const void *residual, const vo
   const int blocks1 = balanced_blocks((I + RG - 1) / RG, MG);
   const int blocks2 = balanced_blocks((d + RD - 1) / RD, MD);
   const bool pdl = env_or("MOM_GEMV_PDL", 1) != 0;     // PDL launches of both GEMVs
-  const int pf = env_or("MOM_GEMV_PREFETCH", 0);        // W_down rows per warp prefetched to L2 first
+  // KB of each warp's first W_down rows prefetched to L2 before waiting for gate/up (0 = off)
+  int pf = env_or("MOM_GEMV_PREFETCH", 0) * 1024;
+  const int row_bytes = I * (BF16 ? 2 : 4);
+  if (pf > row_bytes) pf = row_bytes;
+  pf &= ~15;
   cudaError_t e;
   if ((e = set_smem(gate_up_gemv<BF16, RG, UG, MG>, smem1)) != cudaSuccess) return e;
   if ((e = launch_maybe_pdl(gate_up_gemv<BF16, RG, UG, MG>, blocks1, smem1, stream, pdl, x, wg, wu, h_ws, d, I)) !=
