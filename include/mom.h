@@ -35,8 +35,10 @@
  *               is clamped to cudaOccupancyMaxActiveClusters, since its phase-B tiles wait on
  *               phase-A tiles of other clusters), MOM_EPI_A_COALESCED (1),
  *               MOM_GATHER_FORWARD (1: f1 rows of mini-sequence i-1 forwarded during i),
- *               MOM_GEMV_PDL (1), MOM_GEMV_VARIANT (1: down GEMV with 4 loads in flight per
- *               row at 2 blocks/SM; 0: the earlier 2 at 4/SM), MOM_MLP_PDL (1: programmatic dependent launch between the
+ *               MOM_GEMV_PDL (1: both GEMVs launched with programmatic dependent launch),
+ *               MOM_GEMV_VARIANT (2: down GEMV with 8 loads in flight per row at 2 blocks/SM; 1: 4;
+ *               0: the earlier 2 at 4/SM; 3: also gate/up at 4 per row), MOM_GEMV_PREFETCH (0: KB of
+ *               each warp's first W_down rows prefetched to L2 before the down GEMV waits), MOM_MLP_PDL (1: programmatic dependent launch between the
  *               tcgen05 MLP launches of one call), MOM_HALF_TAIL (1: phase A's last partial wave as
  *               half-width tiles when it fills <= half the clusters), MOM_NB_B (phase-B tile width; default: chosen per shape for
  *               wave quantisation).  None changes results: outputs are bitwise identical.

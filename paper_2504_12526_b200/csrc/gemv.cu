@@ -414,11 +414,12 @@ cudaError_t launch_last_token_mlp(const void *x, const void *residual, const voi
   // 2 x 2 at 4/SM (4 MB in flight: latency-bound at ~3.5 TB/s); measured 74.8 -> 64.5-67.6 us
   // for the pair (profiles/r1_gemv_variants.txt).  MOM_GEMV_VARIANT=0 restores the old shape.
   if (!is_bf16) return last_token_pair<false, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
-  const int variant = gemv::env_or("MOM_GEMV_VARIANT", 1);
+  const int variant = gemv::env_or("MOM_GEMV_VARIANT", 2);
   if (variant == 0)
     return last_token_pair<true, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
   // deeper per-lane load queues (same per-row summation order: bit-neutral): down 8 loads in flight
-  // per row (2), and gate/up 4 per row at 2 blocks/SM as well (3)
+  // per row (2, the default: 69 vs 70 us inside the bench step, profiles/r2_gemv_inbench_ab2.txt), and
+  // gate/up 4 per row at 2 blocks/SM as well (3)
   if (variant == 2)
     return last_token_pair<true, 2, 2, 4, 2, 8, 2>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
   if (variant == 3)
