@@ -51,6 +51,28 @@ def last_token_owner(S_total: int, world: int) -> int:
     return (S_total - 1) // per
 
 
+def early_reload_budget(mode, layers: int, kv_bytes: int, transient_bytes: int) -> int:
+    """f4: bytes of K/V that may be reloaded before the head.  "off" -> 0 (Alg. 1's order); "auto" ->
+    all layers' K/V minus the prefill transient, so the device never holds more than at the end of
+    Alg. 1 (weights + every layer's K/V); an int -> that many bytes."""
+    if mode == "off":
+        return 0
+    if mode == "auto":
+        return max(0, layers * kv_bytes - transient_bytes)
+    b = int(mode)
+    if b < 0:
+        raise ValueError("early_reload budget must be >= 0")
+    return b
+
+
+def early_reload_plan(layers: int, kv_bytes: int, budget: int) -> int:
+    """Number of layers whose reload starts before the head: the first ones, in layer order, while the
+    reloaded bytes fit the budget (each right after its own offload)."""
+    if kv_bytes <= 0:
+        return 0
+    return min(layers, budget // kv_bytes)
+
+
 def gathered_buffer_index(layer: int) -> int:
     """Token-sharded stacks: layer l reads gathered buffer l % 2 and writes buffer (l+1) % 2."""
     return layer % 2
@@ -125,12 +147,8 @@ class PrefillStack:
         # device bytes prefill needs beyond the weights that are not part of Alg. 1's end state
         x_bytes = (2 * world if world > 1 else 1) * S_local * self.d * torch.empty((), dtype=self.dtype).element_size()
         self.transient_bytes = self.ws.numel() + len(self.kv_ring) * self.kv_bytes + x_bytes
-        if early_reload == "off" or not self.reload:
-            self.early_budget = 0
-        elif early_reload == "auto":
-            self.early_budget = max(0, self.L * self.kv_bytes - self.transient_bytes)
-        else:
-            self.early_budget = int(early_reload)
+        self.early_budget = (early_reload_budget(early_reload, self.L, self.kv_bytes, self.transient_bytes)
+                             if self.reload else 0)
         self.h2d = torch.cuda.Stream(device) if self.reload else None
         # the previous run's copies (offload into kv_host, reload out of it) must finish before a new
         # run refills the ring and the host mirrors (pipelined_reload leaves them in flight)

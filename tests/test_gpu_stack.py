@@ -19,7 +19,7 @@ from tests.parity import TOL_BF16, assert_argmax_exact, check_close
 pytestmark = pytest.mark.gpu
 
 
-def _run_stack(cuda_device, d, I, V, L, S, C, d_kv, eps, check_layers, n_rows, offload=True):
+def _run_stack(cuda_device, d, I, V, L, S, C, d_kv, eps, check_layers, n_rows, offload=True, early="off"):
     bf = torch.bfloat16
     weights = [synth.mlp_weights(d, I, l, cuda_device, bf) for l in range(L)]
     wh = synth.head_weight(V, d, cuda_device, bf)
@@ -41,7 +41,8 @@ def _run_stack(cuda_device, d, I, V, L, S, C, d_kv, eps, check_layers, n_rows, o
             if l == L - 1:
                 snaps["last"] = xx[S - 1].cpu()
 
-    stack = PrefillStack(weights, wh, gain, eps, S, C, (S, 2 * d_kv), cuda_device, offload=offload)
+    stack = PrefillStack(weights, wh, gain, eps, S, C, (S, 2 * d_kv), cuda_device, offload=offload,
+                         early_reload=early)
     res = stack.run(x, kv_fill if offload else None, on_layer=on_layer)
     torch.cuda.synchronize()
     errs = {}

@@ -1,7 +1,8 @@
-"""BASELINE config 5 shapes on one GPU: Llama-3-8B MLP at S = 455000 tokens (M = 56 mini-sequences of
-C = 8192, tail 4440 rows), KV [S, 2*1024] bf16 (1.86 GB per layer) offloaded and reloaded.  The stack is
-cut to 4 layers (3 mini-sequence layers + last token) to bound test time; every per-layer step is the
-same as at 32 layers.  Teacher-forced per-layer parity on sampled rows (random, boundaries, tail)."""
+"""BASELINE config 5 on one GPU: Llama-3-8B MLP at S = 455000 tokens (M = 56 mini-sequences of C = 8192,
+tail 4440 rows), KV [S, 2*1024] bf16 (1.86 GB per layer) offloaded and reloaded.  All 32 layers (31
+mini-sequence layers + the last token) with the budgeted early reload (f4) when the host can pin the
+59.6 GB of offloaded K/V, else the first 4 layers.  Teacher-forced per-layer parity on sampled rows
+(random, boundaries, tail), last-token MLP, LM head, exact argmax, offloaded/reloaded bytes."""
 from __future__ import annotations
 
 import pytest
@@ -15,10 +16,11 @@ pytestmark = pytest.mark.gpu
 def test_stack_cfg5_llama_455k_tokens(cuda_device):
     import psutil
     w = synth.CONFIGS[4]
-    L = 4
-    need = L * w.S * 2 * w.d_kv * 2
-    if psutil.virtual_memory().available < 2 * need:
-        pytest.skip(f"host has {psutil.virtual_memory().available / 1e9:.0f} GB free, needs {2 * need / 1e9:.0f} GB")
+    per_layer = w.S * 2 * w.d_kv * 2
+    L = w.layers if psutil.virtual_memory().available >= 1.5 * w.layers * per_layer else 4
+    if psutil.virtual_memory().available < 2 * L * per_layer and L == 4:
+        pytest.skip(f"host has {psutil.virtual_memory().available / 1e9:.0f} GB free")
     assert -(-w.S // w.C) == 56 and w.S - 55 * w.C == 4440
+    checks = [0, L // 2, L - 2] if L > 4 else [0, L - 2]
     _run_stack(cuda_device, w.hidden, w.intermediate, w.vocab, L, w.S, w.C, w.d_kv, w.eps,
-               check_layers=[0, L - 2], n_rows=8)
+               check_layers=checks, n_rows=8, early="auto")
