@@ -196,8 +196,16 @@ class ClockSampler:
                 pass
             time.sleep(self.period)
 
+    def _energy_mj(self):
+        try:
+            return self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h)  # mJ since driver load
+        except Exception:
+            return None
+
     def __enter__(self):
+        self.e0 = self.e1 = None
         if self._ok:
+            self.e0 = self._energy_mj()
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         return self
@@ -206,6 +214,13 @@ class ClockSampler:
         if self._ok:
             self._stop.set()
             self.t.join()
+            self.e1 = self._energy_mj()
+
+    def energy_j(self):
+        """Board energy over the sampled region (NVML total-energy counter), or None."""
+        if self.e0 is None or self.e1 is None:
+            return None
+        return (self.e1 - self.e0) / 1e3
 
     def summary(self):
         if not self._ok:
@@ -694,6 +709,10 @@ def run_mine(args):
         "gpu_launches": n_launch,
     }
     result["clocks"] = clk.summary()
+    ej = clk.energy_j()
+    if ej is not None:  # this GPU's board energy over the headline region (the power cap sets the clock)
+        result["energy"] = {"joules_per_step": ej / args.steps, "tokens_per_joule": wl.S * args.steps / ej,
+                            "note": "NVML total-energy counter around the timed region, this GPU"}
     if world == 1 and cfg.dtype == "bf16":
         try:
             kt = kernel_trace_pass(wl, compute, copy, reload)
