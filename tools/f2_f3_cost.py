@@ -4,7 +4,8 @@ f2 -- the vocab-sharded LM head: time of one rank's shard (V/N rows of W_head + 
 f3 -- the per-layer RMSNorm folded into phase A: config-2 mini-sequence MLP (x + MLP(norm(x))) with the
       gain folded into W_gate/W_up and 1/rms applied in the phase-A epilogue, vs the plain MLP call
       (x + MLP(x)), and vs an unfused torch RMSNorm pass followed by the plain call.
-CUDA events, median of 10 after 3 warm-ups, config 2 shapes."""
+CUDA events (a GPU sleep queued first, so the host's per-call overhead is not in the interval), median of
+10 after 3 warm-ups, config 2 shapes."""
 import json, os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -23,6 +24,7 @@ def timeit(fn, n=10, warm=3):
     ts = []
     for _ in range(n):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(1_000_000)  # the GPU waits while the host enqueues: host call overhead not timed
         e0.record(); fn(); e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
