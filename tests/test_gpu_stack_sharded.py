@@ -1,5 +1,5 @@
 """Token-sharded layer stack (BASELINE config 5's split) at world size 2, as two
-processes on the one GPU of a gpurun box: real cudaIpc handles for both gathered buffers, the f1
+(and 4) processes on the one GPU of a gpurun box: real cudaIpc handles for both gathered buffers, the f1
 peer stores of the phase-B epilogue, a gloo host barrier per layer (comm=None test mode of
 PrefillStack).  Mini-sequences are independent, so every gathered row, the
 last-token MLP output, the logits and the argmax must equal the one-GPU stack's BITWISE (the GPU-only
@@ -100,10 +100,11 @@ def _worker(rank, world, port, cfg, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("S_total", [1536, 1501])
-def test_sharded_stack_equals_one_gpu_bitwise(cuda_device, S_total):
+@pytest.mark.parametrize("world,S_total", [(2, 1536), (2, 1501), (4, 2050)])
+def test_sharded_stack_equals_one_gpu_bitwise(cuda_device, world, S_total):
+    """world 4: every rank stores each output row to 3 peers (and forwards the previous mini-sequence's
+    rows to 3 peers); S_total = 2050 pads the last shard by 2 rows."""
     import torch.multiprocessing as mp
-    world = 2
     cfg = (256, 512, 1000, 4, S_total, 256, 64, 1e-5)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -114,6 +115,6 @@ def test_sharded_stack_equals_one_gpu_bitwise(cuda_device, S_total):
     res = sorted((q.get(timeout=600) for _ in range(world)), key=lambda t: t[0])
     for p in procs:
         p.join(timeout=120)
-    assert res == [(0, True), (1, True)], res
+    assert res == [(r, True) for r in range(world)], res
     for p in procs:
         assert p.exitcode == 0
