@@ -94,6 +94,10 @@ def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     local = 0 if SHARED_GPU else int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 and not dist.is_initialized():
+        # NCCL's init log (transport, NVLS, ranks) on stderr, so a run's communicator setup is on record;
+        # the JSON line on stdout is unaffected
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         backend = "nccl" if torch.cuda.is_available() and args.impl == "mine" and not SHARED_GPU else "gloo"
         if backend == "nccl":
             torch.cuda.set_device(local)
