@@ -369,6 +369,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     }
     a.coalesced_a = static_cast<uint32_t>(env_int("MOM_EPI_A_COALESCED", 1));
     a.fast_silu = static_cast<uint32_t>(env_int("MOM_FAST_SILU", 1));
+    a.epi_hint = static_cast<uint32_t>(env_int("MOM_EPI_L2_HINT", 0));
     a.ready = reinterpret_cast<uint32_t *>(static_cast<char *>(workspace) + h_bytes(S, intermediate, C, dt));
     // f1: every O_i row must reach every peer.  Rows of mini-sequence i-1 (final once its phase B
     // completed) are forwarded by warps 2-3 of this mini-sequence's phase-A launch, so the NVLink

@@ -30,6 +30,7 @@ struct TcMlpArgs {
   uint32_t coalesced_a;      // phase-A epilogue via the smem stage (coalesced H stores)
   uint32_t fast_silu;        // phase-A epilogue SiLU quotient by rcp.approx (MOM_FAST_SILU, default 1)
   unsigned long long *trace; // instrumentation: kMaxTraceCtas x 8 stamps for this launch, or null
+  uint32_t epi_hint;         // MOM_EPI_L2_HINT: bit 0 H stores evict_first, bit 1 phase-B residual/out evict_first
   uint32_t n_peers;          // f1: number of peer destinations (<= kMaxPeers)
   __nv_bfloat16 *peer_out[kMaxPeers];  // f1: peer gathered buffers at this mini-sequence's rows
   const __nv_bfloat16 *fwd_src;        // f1: previous mini-sequence's output rows to forward (or null)

@@ -101,6 +101,10 @@ struct Params {
   uint32_t coalesced_a;          // phase-A epilogue through the smem stage (128-B row segments)
   uint32_t fast_silu;            // phase-A epilogue: quotient of the SiLU by rcp.approx (no branch)
   unsigned long long *trace;     // instrumentation (mom_set_kernel_trace): 8 stamps per CTA, or null
+  // L2 hints for the epilogues' streamed traffic (MOM_EPI_L2_HINT): bit 0 = phase-A H stores
+  // evict_first (H is re-read only by the next launch, and displaces X_i rows that this launch
+  // re-reads), bit 1 = phase-B residual loads and output stores evict_first
+  uint32_t epi_hint;
   uint32_t n_peers;              // f1: extra destinations of the phase-B output rows
   __nv_bfloat16 *peer_out[kMaxPeers];  // f1: peers' gathered buffers, offset like `out`
   // f1 forwarding (warps 2-3): rows [0, fwd_rows) of fwd_src (the previous mini-sequence's
@@ -302,7 +306,12 @@ __device__ __forceinline__ void epilogue_a_coalesced(const Params &p, uint32_t t
                    : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                    : "r"(sw(r, cv))
                    : "memory");
-      if (grow < p.rows && gcol < p.I) *reinterpret_cast<uint4 *>(p.h + size_t(grow) * p.I + gcol) = v;
+      if (grow < p.rows && gcol < p.I) {
+        if (p.epi_hint & 1u)
+          ptx::st_global_v4_hint(p.h + size_t(grow) * p.I + gcol, v, ptx::policy_evict_first());
+        else
+          *reinterpret_cast<uint4 *>(p.h + size_t(grow) * p.I + gcol) = v;
+      }
     }
     __syncwarp();
   }
@@ -335,7 +344,11 @@ __device__ __forceinline__ void epilogue_b(const Params &p, uint32_t taddr, uint
       for (uint32_t i = 0; i < 8; ++i) {
         const uint32_t r = cr + 4 * i, grow = row0_warp + r, gcol = ccol + cv * 8;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (grow < p.rows && gcol < cend) v = *reinterpret_cast<const uint4 *>(p.residual + size_t(grow) * p.d + gcol);
+        if (grow < p.rows && gcol < cend) {
+          const __nv_bfloat16 *src = p.residual + size_t(grow) * p.d + gcol;
+          v = (p.epi_hint & 2u) ? ptx::ld_global_v4_hint(src, ptx::policy_evict_first())
+                                : *reinterpret_cast<const uint4 *>(src);
+        }
         asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sw(r, cv)), "r"(v.x), "r"(v.y), "r"(v.z),
                      "r"(v.w)
                      : "memory");
@@ -380,7 +393,10 @@ __device__ __forceinline__ void epilogue_b(const Params &p, uint32_t taddr, uint
                    : "memory");
       if (grow < p.rows && gcol < cend) {
         const size_t off = size_t(grow) * p.d + gcol;
-        *reinterpret_cast<uint4 *>(p.out + off) = v;
+        if (p.epi_hint & 2u)
+          ptx::st_global_v4_hint(p.out + off, v, ptx::policy_evict_first());
+        else
+          *reinterpret_cast<uint4 *>(p.out + off) = v;
         for (uint32_t k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint4 *>(p.peer_out[k] + off) = v;
       }
     }
@@ -736,6 +752,7 @@ static cudaError_t launch_mode(const TcMlpArgs &a, cudaStream_t stream) {
   p.coalesced_a = a.coalesced_a;
   p.fast_silu = a.fast_silu;
   p.trace = a.trace;
+  p.epi_hint = a.epi_hint;
   p.fwd_src = a.fwd_src;
   p.fwd_rows = a.fwd_rows;
   p.n_fwd = a.fwd_src ? a.n_fwd : 0;

@@ -114,6 +114,20 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
   return p;
 }
 
+// 16-B global store / load with an L2 cache-policy hint (createpolicy descriptor), L1 not allocated
+__device__ __forceinline__ void st_global_v4_hint(void *p, const uint4 &v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_global_v4_hint(const void *p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
 // ------------------------------------------------------------------ tcgen05
 template <int CG>
 __device__ __forceinline__ void tmem_alloc(uint32_t *smem_dst, uint32_t ncols) {
