@@ -69,6 +69,9 @@ def parse_args():
                     help="request i+1 waits for request i's KV reload (no cross-request overlap)")
     ap.add_argument("--gather", choices=["fused", "nccl"], default="fused",
                     help="N>1: all-gather fused into the down-GEMM epilogue (f1) or a separate ncclAllGather")
+    ap.add_argument("--no-tail-overlap", action="store_true",
+                    help="N=1: run request i's last-token tail on the compute stream (no overlap with request "
+                         "i+1's MLP)")
     ap.add_argument("--stack", action="store_true",
                     help="whole layer stack (PrefillStack) of --config (default config 5: Llama-3-8B, 32 layers, "
                          "S = 455000 tokens), token-sharded over the N ranks: strong scaling")
@@ -270,9 +273,24 @@ class Workload:
         self.argmax = torch.empty(1, dtype=torch.int32, device=device)
         self.owns_last = rank == world - 1
         self.comm = None
+        self.tail = None         # enable_tail_overlap(): stream of the last-token tail
         self.peers = []          # f1: peers' gathered buffers (NVLink-mapped), at this rank's rows
         self.peer_maps = []      # (base pointer, offset) to unmap
         self.barrier_scratch = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def enable_tail_overlap(self):
+        """Requests pipelined one step further (one GPU): request i's last-token tail (GEMV pair, LM head,
+        argmax: ~0.25 ms of HBM-bound work) runs on its own stream while request i+1's MLP starts on the
+        compute stream.  The MLP output is double-buffered across requests, and request i+2's MLP waits
+        for request i's tail (it overwrites the rows the tail reads)."""
+        if self.world != 1:
+            return
+        self.tail = torch.cuda.Stream(self.device)
+        self.outs = [self.out, torch.empty_like(self.out)]
+        self.ev_tail_done = [torch.cuda.Event() for _ in range(2)]
+
+    def extra_streams(self):
+        return [self.tail] if self.tail is not None else []
 
     def init_e2e(self, stream):
         """Second device input buffer for the e2e leg: request i streams its rows into slot i % 2
@@ -322,6 +340,9 @@ def run_step(wl, compute, copy, reload, launches, x_host=None, h2d=None, serial=
     from paper_2504_12526_b200 import _mom
     slot = wl.step_index % 2
     wl.step_index += 1
+    if wl.tail is not None:
+        wl.out = wl.outs[slot]
+        compute.wait_event(wl.ev_tail_done[slot])  # request i-2's tail has read these rows
     copy.wait_stream(compute)
     copy.wait_event(wl.ev_reloaded[slot])  # the slot's previous reload has read it
     _mom.kv_offload(wl.kv, wl.kv_host[slot], compute, copy)                             # a9
@@ -355,13 +376,19 @@ def run_step(wl, compute, copy, reload, launches, x_host=None, h2d=None, serial=
         if wl.world > 1:
             _mom.allgather_rows(wl.out, wl.S, wl.comm, wl.rank, wl.world, compute)       # a11 (NCCL)
     launches[0] += 2 * wl.M
+    tail = compute
+    if wl.tail is not None:  # the last-token tail overlaps the next request's MLP
+        tail = wl.tail
+        tail.wait_stream(compute)
     if wl.owns_last:
         last = wl.out[wl.world * wl.S - 1]
         wg1, wu1, wd1 = wl.w1
-        _mom.mlp_last_token(last, last, wg1, wu1, wd1, wl.y, wl.ws_last, compute)        # a6
-        _mom.lm_head_last(wl.y, wl.gain, wl.cfg.eps, wl.wh, wl.logits, wl.argmax, wl.ws_head, compute)  # a7-a8
+        _mom.mlp_last_token(last, last, wg1, wu1, wd1, wl.y, wl.ws_last, tail)           # a6
+        _mom.lm_head_last(wl.y, wl.gain, wl.cfg.eps, wl.wh, wl.logits, wl.argmax, wl.ws_head, tail)  # a7-a8
         launches[0] += 4
-    wl.ev_head[slot].record(compute)  # Alg. 1: the reload follows the head
+    if wl.tail is not None:
+        wl.ev_tail_done[slot].record(tail)
+    wl.ev_head[slot].record(tail)  # Alg. 1: the reload follows the head
     wl.pending_reload = slot
     if serial or x_host is None:
         flush_reload(wl, reload)
@@ -493,7 +520,7 @@ def kernel_trace_pass(wl, compute, copy, reload, steps: int = 2):
         with torch.cuda.stream(compute):
             for _ in range(steps):
                 run_step(wl, compute, copy, reload, [0])
-            join_streams(compute, copy, reload)
+            join_streams(compute, copy, reload, *wl.extra_streams())
     t = kernel_traced(run, steps * 2 * wl.M + 4, wl.device)
     return trace_efficiency(t, wl.S, wl.C, wl.d, wl.I, torch.cuda.get_device_properties(wl.device).multi_processor_count)
 
@@ -567,6 +594,8 @@ def run_mine(args):
     cfg = synth.CONFIGS[args.config]
     peaks, peaks_src = load_peaks()
     wl = Workload(cfg, rank, world, device)
+    if not args.no_tail_overlap and not args.serial:
+        wl.enable_tail_overlap()
     dist_info = {}
     if world > 1:
         if not SHARED_GPU:
@@ -594,7 +623,7 @@ def run_mine(args):
     with torch.cuda.stream(compute):
         for _ in range(args.warmup):
             run_step(wl, compute, copy, reload, dummy, serial=args.serial)
-        join_streams(compute, copy, reload)
+        join_streams(compute, copy, reload, *wl.extra_streams())
     torch.cuda.synchronize()
 
     def timed_steps(serial, timer=None, n_steps=None):
@@ -613,7 +642,7 @@ def run_mine(args):
                 for _ in range(n_steps):
                     run_step(wl, compute, copy, reload, launches if n_steps == args.steps else [0],
                              serial=serial)
-                join_streams(compute, copy, reload)  # every step's offload and reload inside the region
+                join_streams(compute, copy, reload, *wl.extra_streams())  # every copy and tail inside the region
                 e1.record(compute)
                 torch.cuda.synchronize()
         finally:
@@ -728,7 +757,9 @@ def run_mine(args):
             result["kernel_trace"] = {"error": str(e)[:200]}
     result["ms_per_step_event_timed"] = ms_event_timed
     result["config"]["requests"] = ("serial: request i+1 waits for request i's KV reload" if args.serial else
-                                    "pipelined: request i's KV reload (H2D) overlaps request i+1's MLP")
+                                    "pipelined: request i's KV reload (H2D)" +
+                                    (" and last-token tail (GEMVs, LM head)" if wl.tail is not None else "") +
+                                    " overlap request i+1's MLP")
 
     # board energy per step (the power cap sets the clock, so J/token is the efficiency that matters):
     # the NVML energy counter updates too coarsely for the 0.3 s headline region, so a separate pass
@@ -771,10 +802,11 @@ def run_mine(args):
             for _ in range(n):
                 run_step(wl, compute, copy, reload, [0], x_host=x_host, h2d=h2d, serial=args.serial)
                 if wl.owns_last:
-                    lg_host.copy_(wl.logits, non_blocking=True)
-                    am_host.copy_(wl.argmax, non_blocking=True)
+                    with torch.cuda.stream(wl.tail or compute):
+                        lg_host.copy_(wl.logits, non_blocking=True)
+                        am_host.copy_(wl.argmax, non_blocking=True)
             flush_reload(wl, h2d)
-            join_streams(compute, copy, reload, h2d)
+            join_streams(compute, copy, reload, h2d, *wl.extra_streams())
 
         with torch.cuda.stream(compute):
             e2e_steps(args.warmup)  # untimed

@@ -34,30 +34,35 @@ def _reference(wl):
     return out, logits, am
 
 
+@pytest.mark.parametrize("tail", [False, True])
 @pytest.mark.parametrize("e2e", [False, True])
 @pytest.mark.parametrize("serial", [False, True])
-def test_pipelined_steps_equal_one_request(cuda_device, e2e, serial):
+def test_pipelined_steps_equal_one_request(cuda_device, e2e, serial, tail):
     cfg = synth.CONFIGS[1]
     # config-2 shapes with a shorter sequence (3 mini-sequences, ragged tail) to keep the test quick
     small = synth.Workload(cfg.name + "-test", cfg.hidden, cfg.intermediate, 2 * cfg.C + 1000, 3, 32000,
                            cfg.layers, cfg.d_kv, "bf16", cfg.eps, cfg.C)
     wl = bench.Workload(small, 0, 1, cuda_device)
     ref_out, ref_logits, ref_am = _reference(wl)
+    if tail:  # request i's last-token tail on its own stream, overlapping request i+1's MLP
+        wl.enable_tail_overlap()
     compute, copy, reload = (torch.cuda.Stream(cuda_device) for _ in range(3))
     h2d = torch.cuda.Stream(cuda_device)
     x_host = wl.x.cpu().pin_memory() if e2e else None
     if e2e:
         wl.init_e2e(compute)  # double-buffered device input (the second buffer starts empty)
-    wl.out.zero_()
+    for o in (wl.outs if tail else [wl.out]):
+        o.zero_()
     wl.kv_back.zero_()
     with torch.cuda.stream(compute):
         for _ in range(3):
             bench.run_step(wl, compute, copy, reload, [0], x_host=x_host, h2d=h2d if e2e else None, serial=serial)
         if e2e:
             bench.flush_reload(wl, h2d)
-        bench.join_streams(compute, copy, reload, h2d)
+        bench.join_streams(compute, copy, reload, h2d, *wl.extra_streams())
     torch.cuda.synchronize()
-    assert torch.equal(wl.out, ref_out)
+    for o in (wl.outs if tail else [wl.out]):  # 3 requests: both output buffers were written
+        assert torch.equal(o, ref_out)
     assert torch.equal(wl.logits, ref_logits)
     assert int(wl.argmax.item()) == int(ref_am.item())
     assert torch.equal(wl.kv_back, wl.kv)
@@ -74,6 +79,7 @@ def test_bench_step_full_size_vs_oracle(cuda_device):
     from tests.parity import TOL_BF16, assert_argmax_exact, check_close
     cfg = synth.CONFIGS[1]
     wl = bench.Workload(cfg, 0, 1, cuda_device)
+    wl.enable_tail_overlap()  # the bench's default at N = 1
     compute, copy, reload = (torch.cuda.Stream(cuda_device) for _ in range(3))
     h2d = torch.cuda.Stream(cuda_device)
     x_host = wl.x.cpu().pin_memory()
@@ -84,7 +90,7 @@ def test_bench_step_full_size_vs_oracle(cuda_device):
         for _ in range(2):
             bench.run_step(wl, compute, copy, reload, [0], x_host=x_host, h2d=h2d)
         bench.flush_reload(wl, h2d)
-        bench.join_streams(compute, copy, reload, h2d)
+        bench.join_streams(compute, copy, reload, h2d, *wl.extra_streams())
     torch.cuda.synchronize()
     rows = synth.sample_rows(wl.S, wl.C, n_random=32)
     xs = wl.x.cpu()
