@@ -79,7 +79,7 @@ def test_bench_step_full_size_vs_oracle(cuda_device):
     from tests.parity import TOL_BF16, assert_argmax_exact, check_close
     cfg = synth.CONFIGS[1]
     wl = bench.Workload(cfg, 0, 1, cuda_device)
-    wl.enable_tail_overlap()  # the bench's default at N = 1
+    wl.enable_tail_overlap()  # bench.py --tail-overlap (the tests without it cover the default)
     compute, copy, reload = (torch.cuda.Stream(cuda_device) for _ in range(3))
     h2d = torch.cuda.Stream(cuda_device)
     x_host = wl.x.cpu().pin_memory()
