@@ -92,7 +92,7 @@ class StackResult:
     # the final layer's input rows (all N*S_r rows when token-sharded; x itself on one GPU)
     x_final: torch.Tensor | None = None
     copy_stream: torch.cuda.Stream | None = None
-    early_reload_bytes: int = 0  # f4: bytes reloaded before the head (within the device budget)
+    early_reload_bytes: int = 0  # f4: bytes whose reload was enqueued before the head (within the budget)
 
 
 class PrefillStack:
@@ -149,6 +149,9 @@ class PrefillStack:
         self.transient_bytes = self.ws.numel() + len(self.kv_ring) * self.kv_bytes + x_bytes
         self.early_budget = (early_reload_budget(early_reload, self.L, self.kv_bytes, self.transient_bytes)
                              if self.reload else 0)
+        # once the last mini-sequence layer is done, only the last row of x is live and the MLP workspace
+        # is dead: an "auto" budget grows by their bytes for the final layer (Alg. 1)
+        self.final_layer_release = (x_bytes + self.ws.numel()) if (early_reload == "auto" and self.reload) else 0
         self.h2d = torch.cuda.Stream(device) if self.reload else None
         # the previous run's copies (offload into kv_host, reload out of it) must finish before a new
         # run refills the ring and the host mirrors (pipelined_reload leaves them in flight)
@@ -241,16 +244,23 @@ class PrefillStack:
                 src = x if x.shape[0] == self.S else self.shard_of(x)
                 if src.data_ptr() != own.data_ptr():
                     own.copy_(src)
-            def offload_layer(l, slot):                                                        # a9
+            budget = self.early_budget
+
+            def early_reloads(upto):
+                """f4: reload the layers <= upto already offloaded, in order, within the device budget."""
                 nonlocal reloaded
-                _mom.kv_offload(slot, self.kv_host[l], compute, copy, ev_off[l])
-                # f4 early reload of the layers already offloaded, within the device budget
-                while (self.reload and len(reload_done) <= l and
-                       reloaded + self.kv_bytes <= self.early_budget):
+                while self.reload and len(reload_done) <= upto and reloaded + self.kv_bytes <= budget:
                     reload_layer(len(reload_done))
                     reloaded += self.kv_bytes
 
+            def offload_layer(l, slot):                                                        # a9
+                _mom.kv_offload(slot, self.kv_host[l], compute, copy, ev_off[l])
+                early_reloads(l)
+
             for l in range(self.L):
+                if l == self.L - 1 and self.final_layer_release and self.L > 1:
+                    budget += self.final_layer_release  # x (but its last row) and the workspace are dead
+                    early_reloads(self.L - 2)
                 if self.offload:
                     slot = self.kv_ring[l % 2]
                     if l >= 2:
@@ -287,6 +297,7 @@ class PrefillStack:
                     _mom.lm_head_last(self.y, self.gain, self.eps, self.wh, self.logits, self.argmax,
                                       self.ws_head, compute)                                       # a7-a8
                     launches += 4
+            reloaded_before_head = reloaded
             if self.offload and self.defer_last_offload:
                 offload_layer(self.L - 1, self.kv_ring[(self.L - 1) % 2])
             x_final = x if self.world == 1 else self.xbuf[gathered_buffer_index(self.L - 1)]
@@ -302,4 +313,4 @@ class PrefillStack:
                 compute.wait_stream(copy)
         own = self.rank == self.owner
         return StackResult(self.y if own else None, self.logits if own else None, self.argmax if own else None,
-                           self.kv_host, self.kv_dev, launches, reload_done, x_final, copy, reloaded)
+                           self.kv_host, self.kv_dev, launches, reload_done, x_final, copy, reloaded_before_head)

@@ -64,11 +64,11 @@ def test_decode_consumer_waits_per_layer(cuda_device, early):
     kv_bytes = S * 2 * d_kv * 2
     if early == "off":
         assert res.early_reload_bytes == 0
-    elif early == "auto":  # budget = all K/V - (x + workspace + 2 ring slots)
-        expect = (L * kv_bytes - st.transient_bytes) // kv_bytes
-        assert 0 < res.early_reload_bytes == min(expect, L) * kv_bytes
-    else:
-        assert res.early_reload_bytes == L * kv_bytes  # every layer, each right after its offload
+    elif early == "auto":  # budget = all K/V - (x + workspace + 2 ring slots); + x and workspace at the final layer
+        expect = (L * kv_bytes - st.transient_bytes + st.final_layer_release) // kv_bytes
+        assert 0 < res.early_reload_bytes == min(expect, L - 1) * kv_bytes
+    else:  # every layer before the final one (whose offload follows the head), each right after its offload
+        assert res.early_reload_bytes == (L - 1) * kv_bytes
     dec = torch.cuda.Stream()
     rows = torch.arange(0, S, 97, device=cuda_device)
     h = res.y_last.clone()

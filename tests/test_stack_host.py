@@ -28,6 +28,9 @@ def test_early_reload_budget_keeps_peak_at_alg1_end_state():
     assert early_reload_budget("off", L, kv, transient) == 0
     assert early_reload_budget("auto", 2, kv, transient) == 0          # K/V smaller than the transient
     assert early_reload_plan(L, kv, 10 ** 15) == L                     # unlimited: every layer early
+    # the final layer: x (but its last row) and the MLP workspace are dead, two more layers fit
+    x_ws = 455000 * 4096 * 2 + 8192 * 14336 * 2
+    assert early_reload_plan(L - 1, kv, b + x_ws) == 29 and transient - x_ws + 29 * kv <= L * kv
     assert early_reload_budget(5 * kv, L, kv, transient) == 5 * kv
     with pytest.raises(ValueError):
         early_reload_budget(-1, L, kv, transient)
