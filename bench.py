@@ -73,6 +73,8 @@ def parse_args():
                     help="N=1: run request i's last-token tail on its own stream, overlapping request i+1's MLP "
                          "(+0.2-0.9 %% throughput, the tail itself then takes ~1.9 ms instead of ~0.25 ms: "
                          "profiles/r2_tail_overlap_ab.txt)")
+    ap.add_argument("--no-stack", action="store_true",
+                    help="skip the config-5 stack sub-object (stack_cfg5) of the default bench line")
     ap.add_argument("--stack", action="store_true",
                     help="whole layer stack (PrefillStack) of --config (default config 5: Llama-3-8B, 32 layers, "
                          "S = 455000 tokens), token-sharded over the N ranks: strong scaling")
@@ -828,6 +830,11 @@ def run_mine(args):
                          "result_read_back": "the last token's logits + greedy token (Alg. 1 returns L, P:107); "
                                              "the [S, d] MLP output stays in HBM as the next layer's input"}
 
+    # config 5 (the north_star's multi-GPU workload) in the same run: the 32-layer, 455 000-token stack
+    # token-sharded over these N ranks (strong scaling), so every bench run records it too
+    if not args.no_stack and os.environ.get("MOM_BENCH_NO_STACK") != "1":
+        result["stack_cfg5"] = embedded_stack(args, world, rank, device, wl.comm)
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(wl)
     if wl.comm is not None:
@@ -870,39 +877,36 @@ def verify_gathered_rows(st, x_full, weights, x_final, n_per_shard: int = 6):
     return bool(torch.equal(xs, x_final[rows])), len(rows)
 
 
-def run_stack(args):
-    """--stack: Alg. 1 over the whole layer stack of --config (default config 5, Llama-3-8B, 32 layers,
+def stack_host_memory_ok(cfg, layers, world, rank, device):
+    """Every rank of this node pins its shard's offloaded K/V: does the node have room (collective)?"""
+    import psutil
+    from paper_2504_12526_b200.stack import shard_rows
+    per = shard_rows(cfg.S, world, rank)[1]
+    local_ranks = world if SHARED_GPU else int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    need = layers * per * 2 * cfg.d_kv * 2 * local_ranks
+    ok = psutil.virtual_memory().available >= need * 1.15
+    return bool(sum_over_ranks(1.0 if ok else 0.0, world, device) == world), need
+
+
+def measure_stack(args, world, rank, device, comm, config_index, layers, steps, warmup, e2e=True):
+    """Alg. 1 over the whole layer stack of one config (default config 5: Llama-3-8B, 32 layers,
     S = 455000 tokens), token-sharded over the N ranks: per layer each rank runs the
     mini-sequence MLP on its S/N rows, offloads its K/V stand-in to its pinned host mirror, and gathers
     the output rows into every rank's buffer (f1 peer stores + 1 NCCL barrier, or --gather nccl);
-    the rank owning the last token runs the final-layer GEMVs + LM head; every rank reloads its K/V.
-    Strong scaling: value = S_total / (max over ranks of the step time)."""
-    import psutil
+    the rank owning the last token runs the final-layer GEMVs + LM head; every rank reloads its K/V
+    (budgeted early reload, f4, with Alg. 1's order timed beside it).  Strong scaling: value = S_total /
+    (max over ranks of the step time).  Returns the result dict (identical on every rank)."""
     from paper_2504_12526_b200 import _mom
-    from paper_2504_12526_b200 import build as _build
     from paper_2504_12526_b200.stack import PrefillStack, shard_rows
-    world, rank, local = dist_setup(args)
-    if not torch.cuda.is_available():
-        raise SystemExit("bench.py: no CUDA device (the product has no CPU path)")
-    device = torch.device("cuda", local)
-    torch.cuda.set_device(device)
-    if not os.path.exists(_mom.LIB_PATH):
-        _build.build()
-    cfg = synth.CONFIGS[args.config]
+    cfg = synth.CONFIGS[config_index]
     peaks, peaks_src = load_peaks()
     d, I, V, S_total, C = cfg.hidden, cfg.intermediate, cfg.vocab, cfg.S, cfg.C
-    L = args.layers or cfg.layers
+    L = layers or cfg.layers
     start, per, padded = shard_rows(S_total, world, rank)
     bf = torch.bfloat16
     kv_shape = (per, 2 * cfg.d_kv)
-    host_need = L * per * 2 * cfg.d_kv * 2 * (world if SHARED_GPU else 1)
-    if psutil.virtual_memory().available < host_need * 1.15:
-        raise SystemExit(f"bench.py --stack: {host_need / 1e9:.1f} GB of pinned host memory needed for the "
-                         f"offloaded KV, {psutil.virtual_memory().available / 1e9:.1f} GB available (use --layers)")
-    comm = None
     dist_info = {}
-    if world > 1 and not SHARED_GPU:
-        comm = init_nccl(world, rank)
+    if comm is not None:
         dist_info["nccl_comm_nranks"] = _mom.nccl_comm_count(comm)
     gather = args.gather if world > 1 else "fused"
     if SHARED_GPU and gather == "nccl":
@@ -952,7 +956,7 @@ def run_stack(args):
             own.copy_(host if host is not None else x_mine, non_blocking=True)
             return st.run(own, kv_fill, compute, copy)
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         res = step()
     torch.cuda.synchronize()
 
@@ -977,13 +981,13 @@ def run_stack(args):
         return max_over_ranks(e0.elapsed_time(e1) / n, world, device), nl, r
 
     with ClockSampler(device.index) as clk:
-        ms, n_launch, res = timed(args.steps)
+        ms, n_launch, res = timed(steps)
     early_bytes = res.early_reload_bytes
     # the other reload schedule, same run: Alg. 1's order (all reloads after the head) or early
     budget, alt = st.early_budget, None
     st.early_budget = 0 if budget > 0 else max(0, st.L * st.kv_bytes - st.transient_bytes)
     if st.early_budget != budget:
-        a_ms, _, _ = timed(args.steps)
+        a_ms, _, _ = timed(steps)
         alt = {"early_reload_gb": st.early_budget / 1e9, "ms_per_step": a_ms, "value": S_total / (a_ms * 1e-3)}
     st.early_budget = budget
     flops = 6.0 * S_total * d * I * (L - 1)
@@ -994,8 +998,8 @@ def run_stack(args):
     tflops_per_gpu = flops / world / (ms * 1e-3) / 1e12
     result = {
         "metric": "prefill MLP tokens/s (MOM mini-sequence path over the layer stack, token-sharded)",
-        "value": S_total / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "value": S_total / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded random-init weights and inputs, synth/)",
         "config": {"workload": cfg.name + ("" if L == cfg.layers else f"-first{L}layers"), "hidden": d,
                    "intermediate": I, "vocab": V, "layers": L, "global_tokens": S_total, "tokens_per_rank": per,
@@ -1019,11 +1023,11 @@ def run_stack(args):
         "clocks": clk.summary(),
         "shared_gpu_test_mode": SHARED_GPU or None,
     }
-    if not args.no_e2e:
+    if e2e:
         x_host = x_mine.cpu().pin_memory()
         sink = (torch.empty(V, dtype=torch.float32, pin_memory=True), torch.empty(1, dtype=torch.int32,
                                                                                  pin_memory=True))
-        e_ms, _, _ = timed(args.steps, host=x_host, sink=sink)
+        e_ms, _, _ = timed(steps, host=x_host, sink=sink)
         result["e2e"] = {"value": S_total / (e_ms * 1e-3), "unit": "tokens/s",
                          "h2d_bytes_per_step": int(world * per * d * 2), "d2h_bytes_per_step": V * 4 + 4,
                          "ms_per_step": e_ms}
@@ -1032,6 +1036,49 @@ def run_stack(args):
     if dist_info:
         result["distributed"] = dist_info
     st.close()
+    del st, weights, x_full, x_mine, base
+    torch.cuda.empty_cache()
+    return result
+
+
+def embedded_stack(args, world, rank, device, comm):
+    """The config-5 stack measurement (measure_stack, 2 timed steps after 3 warm-ups) as a compact
+    sub-object of the default bench line; skipped (with the reason) if the node cannot pin the K/V."""
+    cfg = synth.CONFIGS[4]
+    ok, need = stack_host_memory_ok(cfg, cfg.layers, world, rank, device)
+    if not ok:
+        return {"skipped": f"{need / 1e9:.1f} GB of pinned host memory needed for the offloaded KV"}
+    r = measure_stack(args, world, rank, device, comm, 4, cfg.layers, steps=2, warmup=3, e2e=False)
+    keep = ("value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "scaling", "gather_verified",
+            "mlp_tflops_per_gpu", "mlp_frac_of_burst_per_gpu", "gpu_launches", "kv_reload", "distributed")
+    out = {k: r[k] for k in keep if k in r}
+    out["workload"] = r["config"]["workload"]
+    out["tokens_per_rank"] = r["config"]["tokens_per_rank"]
+    out["gather"] = r["config"]["gather"]
+    out["sm_mhz"] = r["clocks"].get("sm_mhz")
+    return out
+
+
+def run_stack(args):
+    """--stack: measure_stack on --config (default config 5) as the bench line itself."""
+    from paper_2504_12526_b200 import _mom
+    from paper_2504_12526_b200 import build as _build
+    world, rank, local = dist_setup(args)
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product has no CPU path)")
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    if not os.path.exists(_mom.LIB_PATH):
+        _build.build()
+    cfg = synth.CONFIGS[args.config]
+    L = args.layers or cfg.layers
+    ok, need = stack_host_memory_ok(cfg, L, world, rank, device)
+    if not ok:
+        raise SystemExit(f"bench.py --stack: {need / 1e9:.1f} GB of pinned host memory needed on this node for the "
+                         "offloaded KV (use --layers)")
+    comm = init_nccl(world, rank) if world > 1 and not SHARED_GPU else None
+    result = measure_stack(args, world, rank, device, comm, args.config, L, args.steps, args.warmup,
+                           e2e=not args.no_e2e)
     if comm is not None:
         _mom.nccl_comm_destroy(comm)
     if rank == 0:

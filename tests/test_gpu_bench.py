@@ -24,7 +24,7 @@ def _last_json(out: str) -> dict:
 
 def test_bench_single_gpu_contract(cuda_device):
     r = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"],
-                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+                       cwd=ROOT, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stderr[-3000:]
     res = _last_json(r.stdout)
     for k in REQUIRED:
@@ -41,6 +41,9 @@ def test_bench_single_gpu_contract(cuda_device):
     assert 500 < kt["phaseA_mhz"] <= res["clocks"]["sm_max_mhz"] + 50
     assert 0.8 < kt["mlp_step_mma_issue_efficiency"] <= 1.02
     assert kt["launches"] == 2 * 2 * res["config"]["M"]
+    st = res["stack_cfg5"]  # config 5 (32 layers, 455 000 tokens) measured in the same run
+    assert "skipped" in st or (st["value"] > 0 and st["gather_verified"] is True and st["n_gpus"] == 1
+                               and st["scaling"] == "strong"), st
 
 
 def test_bench_reference_arm():
@@ -55,7 +58,7 @@ def test_bench_two_ranks_shared_gpu(cuda_device):
     env = dict(os.environ, MOM_BENCH_SHARED_GPU="1")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", "29531", "bench.py", "--gpus", "2",
-                        "--steps", "3", "--warmup", "3", "--config", "0"],
+                        "--steps", "3", "--warmup", "3", "--config", "0", "--no-stack"],
                        cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     res = _last_json(r.stdout)
