@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of libmom.so (include/mom.h): argument validation, mini-sequence
 // planning (Alg. 1), TMA descriptor encoding, kernel launches, KV offload/reload
 // (sec. 3.2) and the NCCL all-gather for token-sharded runs.
+#include <nvtx3/nvToolsExt.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -122,10 +123,16 @@ unsigned long long *next_trace_slot(int grid_ctas) {
   return g_trace.buf + (*g_trace.count)++ * (mom::kMaxTraceCtas * 8);
 }
 
+// Every launch of the library is also an NVTX range named after its kind (header-only NVTX v3: a few
+// ns when no tool is attached), so `ncu --nvtx --nvtx-include "mom.phaseA/"` or nsys can select it.
+const char *const kKindNames[] = {"mom.phaseA", "mom.phaseB", "mom.phaseA_f32", "mom.phaseB_f32",
+                                  "mom.last_token_gemv", "mom.lm_head", "mom.mlp_fused"};
+
 struct ScopedTiming {
   cudaStream_t s;
   int64_t slot = -1;
   ScopedTiming(cudaStream_t stream, int kind) : s(stream) {
+    nvtxRangePushA(kind >= 0 && kind < 7 ? kKindNames[kind] : "mom.launch");
     if (g_hook.ev && g_hook.count && *g_hook.count < g_hook.cap) {
       slot = (*g_hook.count)++;
       g_hook.kinds[slot] = kind;
@@ -134,7 +141,14 @@ struct ScopedTiming {
   }
   ~ScopedTiming() {
     if (slot >= 0) cudaEventRecord(g_hook.ev[2 * slot + 1], s);
+    nvtxRangePop();
   }
+};
+
+// NVTX range for the copy / collective entries (no timing slot)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
 };
 
 mom_status_t check_pinned(const void *host, const char *who) {
@@ -755,6 +769,7 @@ mom_status_t mom_kv_offload(const void *kv_dev, void *kv_host_pinned, size_t byt
     cudaEventDestroy(ready);  // released once the recorded work completes
     if (e != cudaSuccess) return cuda_fail(e, "mom_kv_offload: stream ordering");
   }
+  NvtxRange nvtx("mom.kv_offload");
   cudaError_t e = cudaMemcpyAsync(kv_host_pinned, kv_dev, bytes, cudaMemcpyDeviceToHost, cp);
   if (e != cudaSuccess) return cuda_fail(e, "mom_kv_offload: cudaMemcpyAsync D2H");
   if (done) {
@@ -772,6 +787,7 @@ mom_status_t mom_kv_reload(const void *kv_host_pinned, void *kv_dev, size_t byte
   mom_status_t st = check_pinned(kv_host_pinned, "mom_kv_reload");
   if (st != MOM_OK) return st;
   cudaStream_t cp = static_cast<cudaStream_t>(copy_stream);
+  NvtxRange nvtx("mom.kv_reload");
   cudaError_t e = cudaMemcpyAsync(kv_dev, kv_host_pinned, bytes, cudaMemcpyHostToDevice, cp);
   if (e != cudaSuccess) return cuda_fail(e, "mom_kv_reload: cudaMemcpyAsync H2D");
   if (done) {
@@ -922,6 +938,7 @@ mom_status_t mom_allgather_rows(void *rows, int64_t rows_per_rank, int64_t hidde
   const size_t w = dtype_bytes(dt);
   const int nccl_dtype = dt == MOM_BF16 ? 9 /* ncclBfloat16 */ : 7 /* ncclFloat32 */;
   const void *send = static_cast<const char *>(rows) + static_cast<size_t>(rank) * count * w;  // in-place
+  NvtxRange nvtx("mom.allgather_rows");
   int rc = n.allgather(send, rows, count, nccl_dtype, comm, static_cast<cudaStream_t>(stream));
   if (rc != 0) return nccl_fail(rc, "ncclAllGather");
   return nccl_async_check(comm, "ncclAllGather (async)");
@@ -934,6 +951,7 @@ mom_status_t mom_nccl_barrier(void *comm, int32_t *scratch, mom_stream_t stream)
   if (!n.ok) return fail(MOM_ERR_NCCL, "%s", n.why);
   // a 1-element all-reduce on `stream`: no rank's later work starts before every rank's earlier
   // work on its stream (e.g. the peer stores of mom_mlp_minseq_fwd_gather) has completed
+  NvtxRange nvtx("mom.nccl_barrier");
   int rc = n.allreduce(scratch, scratch, 1, 2 /* ncclInt32 */, 0 /* ncclSum */, comm, static_cast<cudaStream_t>(stream));
   if (rc != 0) return nccl_fail(rc, "ncclAllReduce(barrier)");
   return nccl_async_check(comm, "ncclAllReduce(barrier) (async)");

@@ -211,3 +211,12 @@ def test_nccl_failure_entries_reject_bad_arguments(lib):
         _mom.nccl_check(None)
     assert ei.value.status == E
 
+
+
+def test_library_names_its_launches_for_nvtx(lib):
+    """SURVEY §5 tracing: every launch kind is an NVTX range (mom.phaseA, mom.phaseB, ...), selectable with
+    `ncu --nvtx --nvtx-include "mom.phaseA/"`."""
+    blob = open(_mom.LIB_PATH, "rb").read()
+    for name in (b"mom.phaseA", b"mom.phaseB", b"mom.last_token_gemv", b"mom.lm_head", b"mom.kv_offload",
+                 b"mom.kv_reload", b"mom.nccl_barrier"):
+        assert name in blob, name
