@@ -124,6 +124,35 @@ def init_nccl(world: int, rank: int) -> int:
     return comm
 
 
+class NcclWatchdog:
+    """Polls mom_nccl_check (ncclCommGetAsyncError, non-blocking) once a second from a side thread while
+    a multi-GPU run is in flight: a failed or aborted peer makes this rank print the reason and exit
+    instead of blocking forever inside a collective (SURVEY §5 failure detection)."""
+
+    def __init__(self, comm, rank: int, period_s: float = 1.0):
+        self.comm, self.rank, self.period = comm, rank, period_s
+        self._stop = threading.Event()
+
+    def _run(self):
+        from paper_2504_12526_b200 import _mom
+        while not self._stop.wait(self.period):
+            try:
+                _mom.nccl_check(self.comm)
+            except Exception as e:  # noqa: BLE001 -- report and leave: the collective will never finish
+                print(json.dumps({"error": f"rank {self.rank}: NCCL communicator failed: {e}"[:500]}),
+                      file=sys.stderr, flush=True)
+                os._exit(3)
+
+    def __enter__(self):
+        if self.comm is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+
+
 def try_collective(fn, world: int, device):
     """Run fn() on every rank; returns None if it succeeded everywhere, else the first failure's
     reason (every rank learns that some rank failed, so all take the same fallback)."""
@@ -616,6 +645,7 @@ def run_mine(args):
                 args.gather = "nccl"
                 dist_info["gather_fallback_reason"] = why
         dist_info["gather"] = args.gather
+    watchdog = NcclWatchdog(wl.comm, rank).__enter__()
     compute = torch.cuda.Stream(device)
     copy = torch.cuda.Stream(device)
     reload = torch.cuda.Stream(device)
@@ -837,6 +867,7 @@ def run_mine(args):
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(wl)
+    watchdog.__exit__(None, None, None)
     if wl.comm is not None:
         _mom.nccl_check(wl.comm)  # raises if any collective of the run left the communicator in error
     if dist_info:
@@ -1077,8 +1108,9 @@ def run_stack(args):
         raise SystemExit(f"bench.py --stack: {need / 1e9:.1f} GB of pinned host memory needed on this node for the "
                          "offloaded KV (use --layers)")
     comm = init_nccl(world, rank) if world > 1 and not SHARED_GPU else None
-    result = measure_stack(args, world, rank, device, comm, args.config, L, args.steps, args.warmup,
-                           e2e=not args.no_e2e)
+    with NcclWatchdog(comm, rank):
+        result = measure_stack(args, world, rank, device, comm, args.config, L, args.steps, args.warmup,
+                               e2e=not args.no_e2e)
     if comm is not None:
         _mom.nccl_comm_destroy(comm)
     if rank == 0:
