@@ -17,7 +17,6 @@
 #include <cstdlib>
 
 #include "kernels.h"
-#include "ptx.cuh"
 
 namespace mom {
 namespace gemv {
@@ -243,77 +242,6 @@ __global__ void __launch_bounds__(THREADS, MINB) down_gemv(const float *__restri
   }
 }
 
-// Down GEMV fed by bulk copies (bf16): persistent, one block per SM, block b owns rows c = b, b + G, ...
-// of W_down.  A STAGES-deep ring of whole rows in shared memory is filled by cp.async.bulk (the TMA
-// engine: a row's bytes are in flight as ONE request, so the SM keeps STAGES x I x 2 bytes in flight --
-// 196 KB at config 2 -- instead of what its registers can hold), and the first STAGES rows are issued
-// BEFORE griddepcontrol.wait: W_down does not depend on gate/up, so they stream in while gate/up
-// drains.  Thread t owns the 16-B vectors t, t + 256, ... of every row and keeps its slice of h in
-// registers (loaded once), so a row costs only its own bytes of shared-memory reads.  Per row: fixed
-// per-thread order, warp butterfly, warps summed in order (deterministic).
-template <int VPT>
-__global__ void __launch_bounds__(THREADS, 1) down_gemv_bulk(const float *__restrict__ h, const void *__restrict__ wd,
-                                                          const void *__restrict__ residual, void *__restrict__ out,
-                                                          int d, int I, int stages, int stage_stride) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  __shared__ uint64_t bars[16];
-  __shared__ float red[2][WARPS];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int G = gridDim.x, b = blockIdx.x;
-  const int nrows = b < d ? (d - b + G - 1) / G : 0;
-  const uint32_t row_bytes = static_cast<uint32_t>(I) * 2;
-  const char *wdc = static_cast<const char *>(wd);
-  auto issue = [&](int i) {  // row i of this block into stage i % stages
-    const int s = i % stages;
-    ptx::mbar_arrive_expect_tx(&bars[s], row_bytes);
-    ptx::bulk_g2s(smem_raw + static_cast<size_t>(s) * stage_stride, wdc + static_cast<size_t>(b + i * G) * row_bytes,
-                  row_bytes, &bars[s]);
-  };
-  if (tid == 0) {
-    for (int s = 0; s < stages; ++s) ptx::mbar_init(&bars[s], 1);
-    ptx::fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0)
-    for (int i = 0; i < stages && i < nrows; ++i) issue(i);
-  pdl_launch_dependents();  // the LM head may launch early too
-  pdl_wait();               // h (written by gate_up_gemv) is complete and visible from here on
-  const int nvec = I / 8;
-  float hv[VPT][8];
-#pragma unroll
-  for (int k = 0; k < VPT; ++k) {
-    const int v = tid + k * THREADS;
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const float4 f = v < nvec ? __ldg(reinterpret_cast<const float4 *>(h + 8 * v) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-      hv[k][4 * q] = f.x; hv[k][4 * q + 1] = f.y; hv[k][4 * q + 2] = f.z; hv[k][4 * q + 3] = f.w;
-    }
-  }
-  for (int i = 0; i < nrows; ++i) {
-    const int s = i % stages;
-    ptx::mbar_wait(&bars[s], static_cast<uint32_t>((i / stages) & 1));
-    const uint4 *w = reinterpret_cast<const uint4 *>(smem_raw + static_cast<size_t>(s) * stage_stride);
-    float acc = 0.f;
-#pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      const int v = tid + k * THREADS;
-      if (v < nvec) acc += dot8_bf16(w[v], hv[k]);
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) red[i & 1][wid] = acc;
-    __syncthreads();  // every thread is done with stage s; red[i & 1] complete
-    if (tid == 0) {
-      float t = 0.f;
-#pragma unroll
-      for (int q = 0; q < WARPS; ++q) t += red[i & 1][q];
-      const int c = b + i * G;
-      const float rv = residual ? __bfloat162float(static_cast<const __nv_bfloat16 *>(residual)[c]) : 0.f;
-      static_cast<__nv_bfloat16 *>(out)[c] = __float2bfloat16_rn(rv + t);
-      if (i + stages < nrows) issue(i + stages);  // refill the stage just consumed
-    }
-  }
-}
-
 // Order-preserving map float -> uint32 (larger float -> larger key), then pack with the
 // complemented index so that the u64 max picks the largest value and, among equal
 // values, the LOWEST index.
@@ -487,39 +415,6 @@ cudaError_t launch_last_token_mlp(const void *x, const void *residual, const voi
   // for the pair (profiles/r1_gemv_variants.txt).  MOM_GEMV_VARIANT=0 restores the old shape.
   if (!is_bf16) return last_token_pair<false, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
   const int variant = gemv::env_or("MOM_GEMV_VARIANT", 2);
-  if (variant == 4) {  // gate/up as variant 2, down fed by bulk copies (down_gemv_bulk)
-    using namespace gemv;
-    const int row_bytes = I * 2;
-    const int stride = (row_bytes + 127) & ~127;
-    const int vpt = (I / 8 + THREADS - 1) / THREADS;
-    int stages = (200 * 1024) / stride;
-    if (stages > 16) stages = 16;
-    if (stages >= 2 && vpt <= 10) {
-      const size_t smem1 = static_cast<size_t>(d) * sizeof(float);
-      cudaError_t e;
-      if ((e = set_smem(gate_up_gemv<true, 2, 2, 4>, smem1)) != cudaSuccess) return e;
-      const int resident = num_sms * 4 * WARPS;
-      const int groups = (I + 1) / 2, r = (groups + resident - 1) / resident;
-      const int blocks1 = ((groups + r - 1) / r + WARPS - 1) / WARPS;
-      const bool pdl = env_or("MOM_GEMV_PDL", 1) != 0;
-      if ((e = launch_maybe_pdl(gate_up_gemv<true, 2, 2, 4>, blocks1, smem1, stream, pdl, x, wg, wu, h_ws, d, I)) !=
-          cudaSuccess)
-        return e;
-      const size_t smem2 = static_cast<size_t>(stages) * stride;
-      const int blocks2 = d < num_sms ? d : num_sms;
-#define MOM_DOWN_BULK(V)                                                                                      \
-  case V:                                                                                                   \
-    if ((e = set_smem(down_gemv_bulk<V>, smem2)) != cudaSuccess) return e;                                  \
-    return launch_maybe_pdl(down_gemv_bulk<V>, blocks2, smem2, stream, pdl, static_cast<const float *>(h_ws), \
-                            wd, residual, out, d, I, stages, stride);
-      switch (vpt) {
-        MOM_DOWN_BULK(1) MOM_DOWN_BULK(2) MOM_DOWN_BULK(3) MOM_DOWN_BULK(4) MOM_DOWN_BULK(5)
-        MOM_DOWN_BULK(6) MOM_DOWN_BULK(7) MOM_DOWN_BULK(8) MOM_DOWN_BULK(9) MOM_DOWN_BULK(10)
-        default: break;
-      }
-#undef MOM_DOWN_BULK
-    }
-  }
   if (variant == 0)
     return last_token_pair<true, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
   // deeper per-lane load queues (same per-row summation order: bit-neutral): down 8 loads in flight
