@@ -43,7 +43,7 @@ def _kv_fill_for(base, row0):
     return fill
 
 
-def _worker(rank, world, port, cfg, q):
+def _worker(rank, world, port, cfg, q, early="off"):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -66,7 +66,7 @@ def _worker(rank, world, port, cfg, q):
         x_mine[:n_real] = x_full[start:start + n_real]
         base = synth.kv_standin(per, d_kv, 0, dev, bf)
         st = PrefillStack(weights, wh, gain, eps, per, C, (per, 2 * d_kv), dev, world=world, rank=rank,
-                          comm=None, S_total=S_total, gather="fused")
+                          comm=None, S_total=S_total, gather="fused", early_reload=early)
         seen = []
         ok = True
         for rep in range(2):
@@ -100,16 +100,18 @@ def _worker(rank, world, port, cfg, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,S_total", [(2, 1536), (2, 1501), (4, 2050)])
-def test_sharded_stack_equals_one_gpu_bitwise(cuda_device, world, S_total):
+@pytest.mark.parametrize("world,S_total,early", [(2, 1536, "off"), (2, 1501, "off"), (4, 2050, "off"),
+                                                 (2, 1536, 1 << 40)])
+def test_sharded_stack_equals_one_gpu_bitwise(cuda_device, world, S_total, early):
     """world 4: every rank stores each output row to 3 peers (and forwards the previous mini-sequence's
-    rows to 3 peers); S_total = 2050 pads the last shard by 2 rows."""
+    rows to 3 peers); S_total = 2050 pads the last shard by 2 rows; the last case reloads every layer's
+    K/V right after its offload (f4, unlimited budget) on every rank."""
     import torch.multiprocessing as mp
     cfg = (256, 512, 1000, 4, S_total, 256, 64, 1e-5)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q, early)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted((q.get(timeout=600) for _ in range(world)), key=lambda t: t[0])
