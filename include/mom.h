@@ -174,6 +174,14 @@ mom_status_t mom_mlp_last_token(const void *x_last, const void *residual_last, c
                                 const void *w_up, const void *w_down, void *out_last,
                                 int64_t hidden, int64_t intermediate, mom_dtype_t dt,
                                 void *workspace, size_t workspace_bytes, mom_stream_t stream);
+/* f3 on the last token: out_last = x_last + MLP(RMSNorm(x_last) (.) g) with the gain
+ * folded into W_gate / W_up (mom_fold_norm_gain); the gate/up GEMV scales its staged copy of x_last by
+ * r = 1/sqrt(mean(x_last^2) + eps) (the sum of squares comes with the staging pass).  eps >= 0; other
+ * arguments, workspace and errors as mom_mlp_last_token (residual = x_last; out_last may alias it). */
+mom_status_t mom_mlp_last_token_rmsnorm(const void *x_last, const void *w_gate_folded,
+                                        const void *w_up_folded, const void *w_down, void *out_last,
+                                        int64_t hidden, int64_t intermediate, float eps, mom_dtype_t dt,
+                                        void *workspace, size_t workspace_bytes, mom_stream_t stream);
 
 /* ------------------------------------------------------------------------------------
  * a7-a8. LM head on the last token + greedy token.  Alg. 1 P:105 "L = LM_Head(O_last)";

@@ -32,6 +32,7 @@ SIGNATURES = {
     "mom_mlp_minseq_rmsnorm_fwd": (_i32, [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _f32, _i32, _p, _sz, _p]),
     "mom_mlp_last_token_workspace_bytes": (_sz, [_i64]),
     "mom_mlp_last_token": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _p, _sz, _p]),
+    "mom_mlp_last_token_rmsnorm": (_i32, [_p, _p, _p, _p, _p, _i64, _i64, _f32, _i32, _p, _sz, _p]),
     "mom_lm_head_workspace_bytes": (_sz, [_i64]),
     "mom_lm_head_last": (_i32, [_p, _p, _f32, _p, _p, _p, _i64, _i64, _i32, _p, _sz, _p]),
     "mom_lm_head_shard": (_i32, [_p, _p, _f32, _p, _i64, _i64, _p, _p, _i64, _i32, _p, _sz, _p]),
@@ -285,6 +286,21 @@ def mlp_last_token(x_last, residual_last, w_gate, w_up, w_down, out_last, worksp
     _check(lib().mom_mlp_last_token(_ptr(x_last), _ptr(residual_last), _ptr(w_gate), _ptr(w_up), _ptr(w_down),
                                     _ptr(out_last), hidden, I, dt, _ptr(workspace),
                                     workspace.numel() * workspace.element_size(), _stream(stream)))
+    return out_last
+
+
+def mlp_last_token_rmsnorm(x_last, w_gate_folded, w_up_folded, w_down, out_last, eps: float, workspace=None,
+                           stream=None):
+    """f3 on the last token: out_last = x_last + MLP(RMSNorm(x_last) * g), g folded into W_gate/W_up."""
+    _check_gemv(x_last, None, w_gate_folded, w_up_folded, w_down, out_last)
+    hidden = x_last.shape[-1]
+    I = w_gate_folded.shape[0]
+    dt = _dt(x_last)
+    if workspace is None:
+        workspace = torch.empty(lib().mom_mlp_last_token_workspace_bytes(I), dtype=torch.uint8, device=x_last.device)
+    _check(lib().mom_mlp_last_token_rmsnorm(_ptr(x_last), _ptr(w_gate_folded), _ptr(w_up_folded), _ptr(w_down),
+                                            _ptr(out_last), hidden, I, float(eps), dt, _ptr(workspace),
+                                            workspace.numel() * workspace.element_size(), _stream(stream)))
     return out_last
 
 

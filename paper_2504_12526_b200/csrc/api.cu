@@ -647,10 +647,10 @@ size_t mom_mlp_last_token_workspace_bytes(int64_t intermediate) {
   return ((static_cast<size_t>(intermediate) * 4) + 255) & ~static_cast<size_t>(255);  // h, fp32
 }
 
-mom_status_t mom_mlp_last_token(const void *x_last, const void *residual_last, const void *w_gate,
-                                const void *w_up, const void *w_down, void *out_last, int64_t hidden,
-                                int64_t intermediate, mom_dtype_t dt, void *workspace, size_t workspace_bytes,
-                                mom_stream_t stream) {
+static mom_status_t last_token_impl(const void *x_last, const void *residual_last, const void *w_gate,
+                                    const void *w_up, const void *w_down, void *out_last, int64_t hidden,
+                                    int64_t intermediate, mom_dtype_t dt, void *workspace, size_t workspace_bytes,
+                                    mom_stream_t stream, float norm_eps) {
   g_err[0] = 0;
   if (!x_last || !w_gate || !w_up || !w_down || !out_last || !workspace)
     return fail(MOM_ERR_INVALID_ARG, "mom_mlp_last_token: null pointer");
@@ -679,9 +679,27 @@ mom_status_t mom_mlp_last_token(const void *x_last, const void *residual_last, c
   ScopedTiming tm(static_cast<cudaStream_t>(stream), 4);
   e = mom::launch_last_token_mlp(x_last, residual_last, w_gate, w_up, w_down, out_last,
                                              static_cast<float *>(workspace), (int)hidden, (int)intermediate,
-                                             dt == MOM_BF16, num_sms, static_cast<cudaStream_t>(stream));
+                                             dt == MOM_BF16, num_sms, static_cast<cudaStream_t>(stream), norm_eps);
   if (e != cudaSuccess) return cuda_fail(e, "last-token MLP");
   return MOM_OK;
+}
+
+mom_status_t mom_mlp_last_token(const void *x_last, const void *residual_last, const void *w_gate,
+                                const void *w_up, const void *w_down, void *out_last, int64_t hidden,
+                                int64_t intermediate, mom_dtype_t dt, void *workspace, size_t workspace_bytes,
+                                mom_stream_t stream) {
+  return last_token_impl(x_last, residual_last, w_gate, w_up, w_down, out_last, hidden, intermediate, dt, workspace,
+                         workspace_bytes, stream, -1.0f);
+}
+
+mom_status_t mom_mlp_last_token_rmsnorm(const void *x_last, const void *w_gate_folded, const void *w_up_folded,
+                                        const void *w_down, void *out_last, int64_t hidden, int64_t intermediate,
+                                        float eps, mom_dtype_t dt, void *workspace, size_t workspace_bytes,
+                                        mom_stream_t stream) {
+  g_err[0] = 0;
+  if (!(eps >= 0.0f)) return fail(MOM_ERR_INVALID_ARG, "mom_mlp_last_token_rmsnorm: eps must be >= 0");
+  return last_token_impl(x_last, x_last, w_gate_folded, w_up_folded, w_down, out_last, hidden, intermediate, dt,
+                         workspace, workspace_bytes, stream, eps);
 }
 
 size_t mom_lm_head_workspace_bytes(int64_t vocab) {

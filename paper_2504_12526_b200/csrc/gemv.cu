@@ -187,16 +187,29 @@ __device__ __forceinline__ void prefetch_first_rows(const void *base, size_t pit
 
 // h[j] = Swish(sum_k x_k Wg[j,k]) * (sum_k x_k Wu[j,k]), fp32.  Warp-stride over groups of R
 // rows j (gate and up rows of each j streamed together).
+// norm_eps >= 0: the f3 form -- x is first scaled by r = 1/sqrt(mean(x^2) + eps) (the gain is
+// folded into W_gate / W_up by the caller), i.e. h = Swish(Wg' (r x)) (.) (Wu' (r x)).
 template <bool BF16, int R, int U = 2, int MINB = 4>
 __global__ void __launch_bounds__(THREADS, MINB) gate_up_gemv(const void *__restrict__ x, const void *__restrict__ wg,
                                                            const void *__restrict__ wu, float *__restrict__ h, int d,
-                                                           int I) {
+                                                           int I, float norm_eps) {
   pdl_launch_dependents();  // the down GEMV may launch now
   // launched with PDL after the producer of x (the last mini-sequence layer's phase B): the CTAs
   // become resident as that grid's CTAs retire, and wait here for its results
   pdl_wait();
   extern __shared__ float xs[];
-  stage_vec<BF16>(x, xs, d);
+  __shared__ float red[WARPS];
+  float ss = stage_vec<BF16>(x, xs, d);
+  if (norm_eps >= 0.f) {  // fold RMSNorm: the sum of squares came with the staging pass
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int i = 0; i < WARPS; ++i) tot += red[i];
+    const float inv = rsqrtf(tot / static_cast<float>(d) + norm_eps);
+    for (int k = threadIdx.x; k < d; k += THREADS) xs[k] *= inv;
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int w = blockIdx.x * WARPS + (threadIdx.x >> 5);
@@ -376,7 +389,8 @@ static cudaError_t set_smem(K kfn, size_t bytes) {
 
 template <bool BF16, int RG, int UG, int MG, int RD, int UD, int MD>
 static cudaError_t last_token_pair(const void *x, const void *residual, const void *wg, const void *wu, const void *wd,
-                                   void *out, float *h_ws, int d, int I, int num_sms, cudaStream_t stream) {
+                                   void *out, float *h_ws, int d, int I, int num_sms, cudaStream_t stream,
+                                   float norm_eps) {
   using namespace gemv;
   const size_t smem1 = static_cast<size_t>(d) * sizeof(float);
   // Balanced single-wave grids: r = ceil(rows / resident warps) rows per warp, and just enough
@@ -397,8 +411,8 @@ static cudaError_t last_token_pair(const void *x, const void *residual, const vo
   pf &= ~15;
   cudaError_t e;
   if ((e = set_smem(gate_up_gemv<BF16, RG, UG, MG>, smem1)) != cudaSuccess) return e;
-  if ((e = launch_maybe_pdl(gate_up_gemv<BF16, RG, UG, MG>, blocks1, smem1, stream, pdl, x, wg, wu, h_ws, d, I)) !=
-      cudaSuccess)
+  if ((e = launch_maybe_pdl(gate_up_gemv<BF16, RG, UG, MG>, blocks1, smem1, stream, pdl, x, wg, wu, h_ws, d, I,
+                            norm_eps)) != cudaSuccess)
     return e;
   if ((e = launch_maybe_pdl(down_gemv<BF16, RD, UD, MD>, blocks2, 0, stream, pdl, h_ws, wd, residual, out, d, I, pf)) !=
       cudaSuccess)
@@ -408,23 +422,23 @@ static cudaError_t last_token_pair(const void *x, const void *residual, const vo
 
 cudaError_t launch_last_token_mlp(const void *x, const void *residual, const void *wg, const void *wu,
                                   const void *wd, void *out, float *h_ws, int d, int I, bool is_bf16, int num_sms,
-                                  cudaStream_t stream) {
+                                  cudaStream_t stream, float norm_eps) {
   // (rows per warp step, 16-B loads in flight per row, min blocks per SM) for gate/up and down.
   // Down: 2 rows x 4 loads in flight at 2 blocks/SM (2048 warps, 16 MB in flight) instead of
   // 2 x 2 at 4/SM (4 MB in flight: latency-bound at ~3.5 TB/s); measured 74.8 -> 64.5-67.6 us
   // for the pair (profiles/r1_gemv_variants.txt).  MOM_GEMV_VARIANT=0 restores the old shape.
-  if (!is_bf16) return last_token_pair<false, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
+  if (!is_bf16) return last_token_pair<false, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream, norm_eps);
   const int variant = gemv::env_or("MOM_GEMV_VARIANT", 2);
   if (variant == 0)
-    return last_token_pair<true, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
+    return last_token_pair<true, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream, norm_eps);
   // deeper per-lane load queues (same per-row summation order: bit-neutral): down 8 loads in flight
   // per row (2, the default: 69 vs 70 us inside the bench step, profiles/r2_gemv_inbench_ab2.txt), and
   // gate/up 4 per row at 2 blocks/SM as well (3)
   if (variant == 2)
-    return last_token_pair<true, 2, 2, 4, 2, 8, 2>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
+    return last_token_pair<true, 2, 2, 4, 2, 8, 2>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream, norm_eps);
   if (variant == 3)
-    return last_token_pair<true, 2, 4, 2, 2, 8, 2>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
-  return last_token_pair<true, 2, 2, 4, 2, 4, 2>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream);
+    return last_token_pair<true, 2, 4, 2, 2, 8, 2>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream, norm_eps);
+  return last_token_pair<true, 2, 2, 4, 2, 4, 2>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream, norm_eps);
 }
 
 size_t lm_head_partials(int num_sms) { return static_cast<size_t>(num_sms) * 4; }

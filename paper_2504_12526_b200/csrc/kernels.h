@@ -60,9 +60,10 @@ cudaError_t launch_phase_b_f32(const float *h, const float *wd, const float *res
                                int I, cudaStream_t stream);
 
 // GEMV path (gemv.cu).  is_bf16 selects bf16 vs fp32 storage of x/w/out.
+// norm_eps >= 0: x is RMS-normalised first (f3; the gain folded into wg / wu by the caller)
 cudaError_t launch_last_token_mlp(const void *x, const void *residual, const void *wg, const void *wu,
                                   const void *wd, void *out, float *h_ws, int d, int I, bool is_bf16,
-                                  int num_sms, cudaStream_t stream);
+                                  int num_sms, cudaStream_t stream, float norm_eps = -1.0f);
 size_t lm_head_partials(int num_sms);
 cudaError_t launch_lm_head(const void *h, const void *gain, float eps, const void *w, float *logits,
                            int32_t *argmax, unsigned long long *key_out, int vocab_offset,

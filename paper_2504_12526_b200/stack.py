@@ -106,7 +106,8 @@ class PrefillStack:
 
     def __init__(self, weights, w_head, norm_gain, eps, S_local, minseq_len, kv_shape, device,
                  world=1, rank=0, comm=None, S_total=None, offload=True, reload=True, gather="fused",
-                 group=None, pipelined_reload=False, early_reload="off", defer_last_offload=True):
+                 group=None, pipelined_reload=False, early_reload="off", defer_last_offload=True,
+                 norm_gains=None, norm_eps=1e-5):
         self.weights = weights            # list of (w_gate, w_up, w_down), layer 0..L-1
         self.L = len(weights)
         self.wh, self.gain, self.eps = w_head, norm_gain, eps
@@ -117,6 +118,11 @@ class PrefillStack:
         if world > 1 and gather == "nccl" and comm is None:
             raise ValueError("gather='nccl' needs an NCCL communicator")
         self.gather = gather
+        # f3 in the stack: the Llama pre-norm block x + MLP(RMSNorm(x) * g_l) per layer, the gains
+        # folded into W_gate / W_up once here (2 x I x d extra bytes per layer)
+        if norm_gains is not None and world > 1 and gather == "fused":
+            raise ValueError("norm_gains with the fused gather is not supported (use gather='nccl')")
+        self.norm_eps = norm_eps
         self.S_total = S_total if S_total is not None else S_local * world
         if world > 1 and not (world - 1) * S_local < self.S_total <= world * S_local:
             raise ValueError("S_total must satisfy (world-1)*S_local < S_total <= world*S_local")
@@ -125,8 +131,17 @@ class PrefillStack:
         self.dtype = wg0.dtype
         self.I, self.d = wg0.shape
         self.V = w_head.shape[0]
-        self.ws = torch.empty(_mom.mlp_minseq_workspace_bytes(S_local, self.d, self.I, minseq_len, self.dtype),
-                              dtype=torch.uint8, device=device)
+        self.folded = None
+        if norm_gains is not None:
+            if len(norm_gains) != self.L:
+                raise ValueError("one norm gain per layer")
+            self.folded = [(_mom.fold_norm_gain(wg, g), _mom.fold_norm_gain(wu, g))
+                           for (wg, wu, _), g in zip(weights, norm_gains)]
+            ws_bytes = _mom.lib().mom_mlp_minseq_rmsnorm_workspace_bytes(S_local, self.d, self.I, minseq_len,
+                                                                         _mom._dt(wg0))
+        else:
+            ws_bytes = _mom.mlp_minseq_workspace_bytes(S_local, self.d, self.I, minseq_len, self.dtype)
+        self.ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
         self.ws_last = torch.empty(_mom.lib().mom_mlp_last_token_workspace_bytes(self.I), dtype=torch.uint8,
                                    device=device)
         self.ws_head = torch.empty(_mom.lib().mom_lm_head_workspace_bytes(self.V), dtype=torch.uint8, device=device)
@@ -276,24 +291,31 @@ class PrefillStack:
                 if on_layer is not None:
                     on_layer(l, cur)
                 wg, wu, wd = self.weights[l]
+                if self.folded is not None:
+                    wg, wu = self.folded[l]
                 if l < self.L - 1:
-                    if self.world == 1:
-                        _mom.mlp_minseq_fwd(x, x, wg, wu, wd, x, self.C, self.ws, compute)          # a1-a5
+                    src = x if self.world == 1 else self.shard_of(cur)
+                    dst = x if self.world == 1 else self.shard_of(self.xbuf[gathered_buffer_index(l + 1)])
+                    if self.folded is not None:                                                    # + f3
+                        _mom.mlp_minseq_rmsnorm_fwd(src, wg, wu, wd, dst, self.C, self.norm_eps, self.ws, compute)
+                    elif self.world > 1 and self.gather == "fused":                                # a11 fused (f1)
+                        _mom.mlp_minseq_fwd_gather(src, src, wg, wu, wd, dst,
+                                                   self.peers[gathered_buffer_index(l + 1)], self.C, self.ws, compute)
                     else:
-                        nxt_i = gathered_buffer_index(l + 1)
-                        src, dst = self.shard_of(cur), self.shard_of(self.xbuf[nxt_i])
-                        if self.gather == "fused":                                                 # a11 fused (f1)
-                            _mom.mlp_minseq_fwd_gather(src, src, wg, wu, wd, dst, self.peers[nxt_i], self.C,
-                                                       self.ws, compute)
+                        _mom.mlp_minseq_fwd(src, src, wg, wu, wd, dst, self.C, self.ws, compute)    # a1-a5
+                    if self.world > 1:
+                        if self.gather == "fused":
                             self._barrier(compute)
                         else:
-                            _mom.mlp_minseq_fwd(src, src, wg, wu, wd, dst, self.C, self.ws, compute)
-                            _mom.allgather_rows(self.xbuf[nxt_i], self.S, self.comm, self.rank, self.world,
-                                                compute)                                           # a11 (NCCL)
+                            _mom.allgather_rows(self.xbuf[gathered_buffer_index(l + 1)], self.S, self.comm,
+                                                self.rank, self.world, compute)                    # a11 (NCCL)
                     launches += 2 * math.ceil(self.S / self.C)
                 elif self.rank == self.owner:
                     last = cur[self.S_total - 1]
-                    _mom.mlp_last_token(last, last, wg, wu, wd, self.y, self.ws_last, compute)     # a6
+                    if self.folded is not None:                                                    # a6 + f3
+                        _mom.mlp_last_token_rmsnorm(last, wg, wu, wd, self.y, self.norm_eps, self.ws_last, compute)
+                    else:
+                        _mom.mlp_last_token(last, last, wg, wu, wd, self.y, self.ws_last, compute)  # a6
                     _mom.lm_head_last(self.y, self.gain, self.eps, self.wh, self.logits, self.argmax,
                                       self.ws_head, compute)                                       # a7-a8
                     launches += 4

@@ -357,3 +357,24 @@ def test_rmsnorm_folded_mlp(cuda_device, S, d, I, C):
     _mom.mlp_minseq_rmsnorm_fwd(gx, wg_f, wu_f, G(wd), gx, C, eps)  # in place
     torch.cuda.synchronize()
     assert torch.equal(gx, out)
+
+
+@pytest.mark.parametrize("d,I", [(4096, 14336), (520, 1160)])
+def test_last_token_rmsnorm_vs_oracle(cuda_device, d, I):
+    """f3 on the last token (mom_mlp_last_token_rmsnorm): out = x + MLP(RMSNorm(x) * g) with g folded into
+    W_gate / W_up and the norm applied to the GEMV's staged x; against the oracle's literal norm-then-MLP
+    (S:126), and equal to the tcgen05 folded-norm path's row within the bf16 bar."""
+    bf = torch.bfloat16
+    wg, wu, wd = synth.mlp_weights(d, I, 0, "cpu", bf)
+    gain = synth.norm_gain(d, "cpu", bf)
+    x = (synth.hidden(3, d, "cpu", torch.float32) * 3.0).to(bf)
+    G = lambda t: t.to(cuda_device)  # noqa: E731
+    wg_f, wu_f = _mom.fold_norm_gain(G(wg), G(gain)), _mom.fold_norm_gain(G(wu), G(gain))
+    for eps in (1e-5, 3.0):
+        y = torch.empty(d, dtype=bf, device=cuda_device)
+        _mom.mlp_last_token_rmsnorm(G(x)[2], wg_f, wu_f, G(wd), y, eps)
+        torch.cuda.synchronize()
+        ref = oracle.mlp_norm_rows(x, gain, eps, wg, wu, wd, [2])[0]
+        check_close(y.cpu(), ref, TOL_BF16, f"last-token rmsnorm d={d} I={I} eps={eps}")
+    with pytest.raises(_mom.MomError):
+        _mom.mlp_last_token_rmsnorm(G(x)[2], wg_f, wu_f, G(wd), y, -1.0)

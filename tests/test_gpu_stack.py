@@ -184,3 +184,40 @@ def test_argmax_allreduce_nccl_single_rank(cuda_device):
     torch.cuda.synchronize()
     _mom.nccl_comm_destroy(comm)
     assert int(am.item()) == int(ref.item())
+
+
+def test_stack_with_folded_rmsnorm(cuda_device):
+    """f3 inside the layer loop: every layer is the Llama pre-norm MLP half x + MLP(RMSNorm(x) * g_l)
+    (S:260), mini-sequence layers through mom_mlp_minseq_rmsnorm_fwd and the last token through
+    mom_mlp_last_token_rmsnorm.  Teacher-forced per layer against the oracle's literal norm-then-MLP, the
+    last token too; the LM head and argmax on the GPU's own final hidden vector."""
+    d, I, V, L, S, C, eps = 256, 512, 1000, 4, 700, 256, 1e-5
+    bf = torch.bfloat16
+    weights = [synth.mlp_weights(d, I, l, cuda_device, bf) for l in range(L)]
+    gains = [(synth.norm_gain(d, cuda_device, torch.float32) * (1.0 + 0.1 * l)).to(bf) for l in range(L)]
+    wh = synth.head_weight(V, d, cuda_device, bf)
+    gain_f = synth.norm_gain(d, cuda_device, bf)
+    x = (synth.hidden(S, d, cuda_device, torch.float32) * 3.0).to(bf)  # un-normed residual stream
+    rows = synth.sample_rows(S, C, n_random=48)
+    snaps = {}
+
+    def on_layer(l, xx):
+        snaps[l] = xx[rows].cpu()
+        if l == L - 1:
+            snaps["last"] = xx[S - 1].cpu()
+
+    st = PrefillStack(weights, wh, gain_f, eps, S, C, (S, 128), cuda_device, offload=False, norm_gains=gains,
+                      norm_eps=eps)
+    res = st.run(x, on_layer=on_layer)
+    torch.cuda.synchronize()
+    for l in range(L - 1):
+        wg, wu, wd = (t.cpu() for t in weights[l])
+        ref = oracle.mlp_norm_rows(snaps[l], gains[l].cpu(), eps, wg, wu, wd, list(range(len(rows))))
+        check_close(snaps[l + 1], ref, TOL_BF16, f"normed layer {l} (teacher-forced)")
+    wg, wu, wd = (t.cpu() for t in weights[L - 1])
+    ref_y = oracle.mlp_norm_rows(snaps["last"][None], gains[L - 1].cpu(), eps, wg, wu, wd, [0])[0]
+    check_close(res.y_last.cpu(), ref_y, TOL_BF16, "normed last token")
+    yn = oracle.rmsnorm(res.y_last.cpu().double().numpy(), gain_f.cpu(), eps)
+    ref_logits = oracle.lm_head(yn, wh.cpu())[0]
+    check_close(res.logits.cpu(), ref_logits, 1e-4, "LM head (normed stack)")
+    assert_argmax_exact(int(res.argmax.item()), ref_logits, "normed stack head")
