@@ -32,6 +32,14 @@ torch.cuda.synchronize()
 assert torch.equal(out_f, out) and all(torch.equal(p[S:2 * S], out) for p in peers + [mine])
 y = torch.empty(d, dtype=bf, device=dev)
 _mom.mlp_last_token(out[-1], out[-1], wg, wu, wd, y)
+# f3: folded RMSNorm in the MLP and in the last-token GEMV
+g = synth.norm_gain(d, dev, bf)
+wgf, wuf = _mom.fold_norm_gain(wg, g), _mom.fold_norm_gain(wu, g)
+out_n = torch.empty_like(x)
+_mom.mlp_minseq_rmsnorm_fwd(x, wgf, wuf, wd, out_n, C, 1e-5)
+y_n = torch.empty(d, dtype=bf, device=dev)
+_mom.mlp_last_token_rmsnorm(x[-1], wgf, wuf, wd, y_n, 1e-5)
+torch.cuda.synchronize()
 wh = synth.head_weight(1000, d, dev, bf)
 logits = torch.empty(1000, dtype=torch.float32, device=dev)
 am = torch.empty(1, dtype=torch.int32, device=dev)
