@@ -435,6 +435,7 @@ mom_status_t run_minseq(const void *x, const void *residual, const void *w_gate,
     }
     if (e != cudaSuccess) return cuda_fail(e, "phase A (tcgen05)");
     a.group_m = group_b;
+    a.group_n = static_cast<uint32_t>(env_int("MOM_RASTER_B_COLS", 0));
     a.fwd_src = nullptr;  // forwarding rides on the phase-A launch only
     a.n_fwd = 0;
     a.pdl = mlp_pdl;

@@ -39,6 +39,7 @@ struct TcMlpArgs {
   uint32_t nb;               // phase-B tile width (multiple of 32, <= 256; 0 = 256); W_down map box = nb/2 rows
   int cta_group;             // 1 or 2
   uint32_t group_m;          // raster group (0 = default)
+  uint32_t group_n;          // phase B column-group raster (0 = row groups)
   bool pdl;                  // launch with programmatic stream serialization (split mode)
   uint32_t policy;           // TMA L2 cache policy variant (0 = default)
   int num_sms;

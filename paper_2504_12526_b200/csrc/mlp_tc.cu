@@ -88,6 +88,7 @@ struct Params {
   uint32_t nA, nB;       // N tiles of phase A (I/128) and phase B (d/nb)
   uint32_t nb;           // phase-B tile width (UMMA N, multiple of 32, <= 256), chosen for wave quantisation
   uint32_t group_m;      // raster: row blocks per group (N iterates inside a group)
+  uint32_t group_n;      // phase B only, if > 0: column-block groups instead (M iterates inside a group)
   uint32_t policy;       // TMA L2 policy: 0 reuse-aware (default), 1 all evict_normal, 2 A evict_first
   // Phase-A wave-tail split (MODE_A): tiles [0, n_full) are the usual 128-column tiles; the R tiles
   // that would form the last, partial wave are instead 2R half-width (64-column) tiles, so the last
@@ -179,6 +180,19 @@ __device__ __forceinline__ Tile decode_tile(uint32_t t, const Params &p) {
     tl.a = a;
     tl.m = g * G + local % gm;
     tl.n = local / gm;
+  } else if (MODE == MODE_B && p.group_n > 0) {
+    // column-block groups: GN output-column panels of W_down stay hot while all row blocks of H_i
+    // stream past them (tools/l2_model_phase_b.py: ~10 % fewer DRAM reads at GN = 8)
+    const uint32_t GN = p.group_n;
+    const uint32_t per_group = GN * p.m_tiles;
+    const uint32_t g = t / per_group;
+    const uint32_t local = t - g * per_group;
+    const uint32_t n0 = g * GN;
+    uint32_t gn = p.nB - n0;
+    if (gn > GN) gn = GN;
+    tl.n = n0 + local % gn;
+    tl.m = local / gn;
+    tl.a = false;
   } else {
     const uint32_t nt = MODE == MODE_A ? p.nA : p.nB;
     const uint32_t per_group = G * nt;
@@ -729,6 +743,7 @@ static cudaError_t launch_mode(const TcMlpArgs &a, cudaStream_t stream) {
   uint32_t g = a.group_m ? a.group_m : (MODE == MODE_B ? 8 : 16);
   if (g > p.m_tiles) g = p.m_tiles;
   p.group_m = g;
+  p.group_n = MODE == MODE_B ? (a.group_n < p.nB ? a.group_n : p.nB) : 0;
   p.policy = a.policy;
   // phase-A wave tail: T tiles on `clusters` persistent clusters leave R = T mod clusters tiles for
   // a last partial wave; when 2R <= clusters they run as 2R half-width tiles (half a tile time)

@@ -19,7 +19,8 @@ KNOBS = [{}, {"MOM_CTA_GROUP": "1"}, {"MOM_GROUP_M_A": "1"}, {"MOM_GROUP_M_A": "
          {"MOM_NB_B": "224", "MOM_CTA_GROUP": "1"}, {"MOM_NB_B": "192", "MOM_FUSED": "1"}, {"MOM_MLP_PDL": "0"},
          {"MOM_MLP_PDL": "0", "MOM_CTA_GROUP": "1"}, {"MOM_HALF_TAIL": "0"}, {"MOM_HALF_TAIL": "0", "MOM_CTA_GROUP": "1"},
          {"MOM_EPI_L2_HINT": "0"}, {"MOM_EPI_L2_HINT": "1"}, {"MOM_EPI_L2_HINT": "3"},
-         {"MOM_EPI_L2_HINT": "3", "MOM_CTA_GROUP": "1"}, {"MOM_EPI_L2_HINT": "1", "MOM_GROUP_M_A": "32"}]
+         {"MOM_EPI_L2_HINT": "3", "MOM_CTA_GROUP": "1"}, {"MOM_EPI_L2_HINT": "1", "MOM_GROUP_M_A": "32"},
+         {"MOM_RASTER_B_COLS": "1"}, {"MOM_RASTER_B_COLS": "3"}, {"MOM_RASTER_B_COLS": "8", "MOM_CTA_GROUP": "1"}]
 ALL = sorted({k for v in KNOBS for k in v})
 
 
