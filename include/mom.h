@@ -41,7 +41,9 @@
  *               each warp's first W_down rows prefetched to L2 before the down GEMV waits), MOM_MLP_PDL (1: programmatic dependent launch between the
  *               tcgen05 MLP launches of one call), MOM_HALF_TAIL (1: phase A's last partial wave as
  *               half-width tiles when it fills <= half the clusters), MOM_NB_B (phase-B tile width; default: chosen per shape for
- *               wave quantisation), MOM_EPI_L2_HINT (0; bit 0: phase-A H stores evict_first, bit 1:
+ *               wave quantisation), MOM_RASTER_B_COLS (0: phase-B raster by row-block groups; G > 0:
+ *               by groups of G output-column blocks -- 10 % fewer DRAM reads at G = 8, no measured
+ *               step gain), MOM_EPI_L2_HINT (0; bit 0: phase-A H stores evict_first, bit 1:
  *               phase-B residual loads / output stores evict_first -- measured, no gain).
  *               None changes results: outputs are bitwise identical.
  *               Numerics knob: MOM_FAST_SILU (1: the phase-A SiLU quotient by rcp.approx, <= 2 fp32
