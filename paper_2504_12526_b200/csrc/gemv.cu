@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(THREADS, 4) lm_head_gemv(const void *__restric
   __shared__ float red[WARPS];
   __shared__ unsigned long long best_s[WARPS];
   pdl_wait();  // h comes from the previous kernel (PDL launch; a no-op without the attribute)
+  pdl_launch_dependents();  // argmax_reduce may launch now (it waits for this grid's partials)
   // prologue: fp32 copy of h and (optionally) the final RMSNorm
   float ss = stage_vec<BF16>(hin, hs, d);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -330,6 +331,7 @@ __global__ void __launch_bounds__(THREADS, 4) lm_head_gemv(const void *__restric
 __global__ void argmax_reduce(const unsigned long long *__restrict__ partials, int n, int32_t *__restrict__ out,
                               unsigned long long *__restrict__ key_out) {
   __shared__ unsigned long long s[32];
+  pdl_wait();  // launched with PDL behind lm_head_gemv: its partials are complete from here on
   unsigned long long b = 0ull;
   for (int i = threadIdx.x; i < n; i += blockDim.x) b = partials[i] > b ? partials[i] : b;
   b = warp_max_u64(b);
@@ -357,6 +359,25 @@ static cudaError_t launch_pdl(void (*kfn)(KArgs...), int blocks, size_t smem, cu
   cfg.gridDim = dim3(blocks, 1, 1);
   cfg.blockDim = dim3(THREADS, 1, 1);
   cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kfn, static_cast<KArgs>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_maybe_pdl_threads(void (*kfn)(KArgs...), int blocks, int threads, cudaStream_t stream,
+                                            bool pdl, Args... args) {
+  if (!pdl) {
+    kfn<<<blocks, threads, 0, stream>>>(static_cast<KArgs>(args)...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -466,8 +487,9 @@ cudaError_t launch_lm_head(const void *h, const void *gain, float eps, const voi
     e = launch_pdl(lm_head_gemv<false, R, U>, blocks, smem, stream, h, gain, eps, w, logits, partials, d, V, vocab_offset);
   }
   if (e != cudaSuccess) return e;
-  argmax_reduce<<<1, 1024, 0, stream>>>(partials, blocks, argmax, key_out);
-  return cudaGetLastError();
+  // PDL: the reduction's launch overlaps the head's tail; it waits in griddepcontrol.wait
+  return launch_maybe_pdl_threads(argmax_reduce, 1, 1024, stream, env_or("MOM_GEMV_PDL", 1) != 0, partials, blocks,
+                                  argmax, key_out);
 }
 
 cudaError_t launch_key_to_index(const unsigned long long *key, int32_t *argmax, cudaStream_t stream) {
