@@ -29,23 +29,27 @@
  *               (arguments are checked before any launch).  MOM_ERR_CUDA / _NCCL report a failed
  *               launch or library call; launches of the same call that preceded it (earlier
  *               mini-sequences) stay enqueued.  mom_last_error() returns a thread-local message.
- *   Tuning      Environment knobs read per call (defaults are the measured best on B200):
- *               MOM_CTA_GROUP (2), MOM_GROUP_M_A (16), MOM_GROUP_M_B (8), MOM_TMA_POLICY (0),
- *               MOM_FUSED (0: two launches per mini-sequence; 1: one persistent launch whose grid
- *               is clamped to cudaOccupancyMaxActiveClusters, since its phase-B tiles wait on
- *               phase-A tiles of other clusters), MOM_EPI_A_COALESCED (1),
- *               MOM_GATHER_FORWARD (1: f1 rows of mini-sequence i-1 forwarded during i),
- *               MOM_GEMV_PDL (1: both GEMVs launched with programmatic dependent launch),
- *               MOM_GEMV_VARIANT (2: down GEMV with 8 loads in flight per row at 2 blocks/SM; 1: 4;
- *               0: the earlier 2 at 4/SM; 3: also gate/up at 4 per row), MOM_GEMV_PREFETCH (0: KB of
- *               each warp's first W_down rows prefetched to L2 before the down GEMV waits), MOM_MLP_PDL (1: programmatic dependent launch between the
- *               tcgen05 MLP launches of one call), MOM_HALF_TAIL (1: phase A's last partial wave as
- *               half-width tiles when it fills <= half the clusters), MOM_NB_B (phase-B tile width; default: chosen per shape for
- *               wave quantisation), MOM_RASTER_B_COLS (0: phase-B raster by row-block groups; G > 0:
- *               by groups of G output-column blocks -- 10 % fewer DRAM reads at G = 8, no measured
- *               step gain), MOM_EPI_L2_HINT (0; bit 0: phase-A H stores evict_first, bit 1:
- *               phase-B residual loads / output stores evict_first -- measured, no gain).
- *               None changes results: outputs are bitwise identical.
+ *   Tuning      Environment knobs read per call (defaults are the measured best on B200).  None
+ *               changes results -- outputs are bitwise identical for every setting (knob tests):
+ *               MOM_CTA_GROUP (2)        CTAs per tcgen05 tile (cta_group::2 pair, or 1)
+ *               MOM_GROUP_M_A (16), MOM_GROUP_M_B (8)   raster: row blocks per group
+ *               MOM_RASTER_B_COLS (0)    phase B by groups of G output-column blocks instead
+ *                                        (10 % fewer DRAM reads at G = 8, no measured step gain)
+ *               MOM_TMA_POLICY (0)       TMA L2 cache-policy variant of the operand loads
+ *               MOM_EPI_L2_HINT (0)      bit 0: H stores evict_first; bit 1: phase-B residual
+ *                                        loads / output stores evict_first (measured, no gain)
+ *               MOM_FUSED (0)            1: both phases in one persistent launch, grid clamped to
+ *                                        cudaOccupancyMaxActiveClusters (phase-B tiles wait on
+ *                                        phase-A tiles of other clusters)
+ *               MOM_EPI_A_COALESCED (1)  phase-A epilogue through a swizzled smem stage
+ *               MOM_MLP_PDL (1)          programmatic dependent launch between the MLP launches
+ *               MOM_HALF_TAIL (1)        phase A's last partial wave as half-width tiles
+ *               MOM_NB_B (per shape)     phase-B tile width (wave quantisation)
+ *               MOM_GATHER_FORWARD (1)   f1: rows of mini-sequence i-1 forwarded during i
+ *               MOM_GEMV_PDL (1)         both last-token GEMVs and the argmax reduction PDL-launched
+ *               MOM_GEMV_VARIANT (2)     down GEMV loads in flight per row: 2 -> 8 at 2 blocks/SM,
+ *                                        1 -> 4, 0 -> 2 at 4 blocks/SM; 3 -> also gate/up at 4
+ *               MOM_GEMV_PREFETCH (0)    KB of each warp's first W_down rows prefetched to L2
  *               Numerics knob: MOM_FAST_SILU (1: the phase-A SiLU quotient by rcp.approx, <= 2 fp32
  *               ulp; 0: IEEE division, whose per-element slow-path branch serialises the epilogue).
  *   Alignment   Device pointers must be 16-byte aligned and row pitches (hidden*w,
