@@ -951,8 +951,15 @@ def measure_stack(args, world, rank, device, comm, config_index, layers, steps, 
     x_mine[:n_real] = x_full[start:start + n_real]
     base = synth.kv_standin(per, cfg.d_kv, 0, device, bf)
 
-    def kv_fill(l, slot):  # attention stand-in: this rank's K/V rows of layer l
-        slot.copy_(base)
+    filled = set()
+
+    def kv_fill(l, slot):  # attention stand-in: layer l's K/V rows -- the seeded stand-in, written
+        # into each ring slot once, with the layer id stamped into column 0 (attention itself is out of
+        # scope; the offload still copies every byte of the slot)
+        if slot.data_ptr() not in filled:
+            slot.copy_(base)
+            filled.add(slot.data_ptr())
+        slot.view(torch.int16)[:, 0] = l
 
     st = None
     if world > 1 and gather == "fused":
