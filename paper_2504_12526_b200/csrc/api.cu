@@ -235,9 +235,9 @@ mom_status_t mom_set_kernel_trace(void *dev_buf, int64_t capacity, int64_t *coun
 }
 
 const char *mom_version(void) {
-  return "libmom 0.3 sm_100a: tcgen05 2-CTA SwiGLU MLP (phase A/B, half-width tail tiles, fused option), fused "
-         "all-gather stores, folded RMSNorm, SIMT f32, PDL GEMVs + argmax, vocab-sharded head, KV copies, host-input "
-         "prefetch, NCCL, in-kernel trace";
+  return "libmom 0.4 sm_100a: tcgen05 2-CTA SwiGLU MLP (phase A/B, half-width tail tiles, fused option), fused "
+         "all-gather stores, folded RMSNorm (MLP and last token), SIMT f32, PDL GEMVs + argmax, vocab-sharded head, "
+         "KV copies, host-input prefetch, NCCL with async-error checks, in-kernel trace, NVTX ranges";
 }
 
 int64_t mom_plan_minseq(int64_t S, int64_t C, int64_t *starts, int64_t *lens, int64_t cap) {
