@@ -42,6 +42,7 @@ def test_bench_single_gpu_contract(cuda_device):
     assert 0.8 < kt["mlp_step_mma_issue_efficiency"] <= 1.02
     assert kt["launches"] == 2 * 2 * res["config"]["M"]
     st = res["stack_cfg5"]  # config 5 (32 layers, 455 000 tokens) measured in the same run
+    assert "error" not in st, st
     assert "skipped" in st or (st["value"] > 0 and st["gather_verified"] is True and st["n_gpus"] == 1
                                and st["scaling"] == "strong"), st
 
