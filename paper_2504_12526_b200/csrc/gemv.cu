@@ -255,6 +255,54 @@ __global__ void __launch_bounds__(THREADS, MINB) down_gemv(const float *__restri
   }
 }
 
+// K-split down GEMV (bf16): KS consecutive warps of a block share R rows; warp q sums the 16-B vectors
+// of its slice [q n / KS, (q+1) n / KS) of each row, and the KS partial sums are added in q order through
+// shared memory (a fixed order: deterministic).  Each warp's chain of dependent loads is KS times
+// shorter and KS times more warps stream at once than in down_gemv, for the same rows.  The loop trip
+// count is uniform across the block (block-wide barriers inside).
+template <int R, int U, int KS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) down_gemv_ks(const float *__restrict__ h, const void *__restrict__ wd,
+                                                           const void *__restrict__ residual, void *__restrict__ out,
+                                                           int d, int I) {
+  constexpr int GPB = WARPS / KS;  // row groups per block
+  __shared__ float part[WARPS][R];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int grp = wid / KS, q = wid % KS;
+  const int nvec = I / 8;
+  const int v_lo = q * nvec / KS, v_hi = (q + 1) * nvec / KS;
+  const size_t pitch = static_cast<size_t>(I) * 2;
+  const int stride = gridDim.x * GPB * R;
+  const int iters = (d + stride - 1) / stride;
+  pdl_launch_dependents();  // the LM head may launch early too
+  pdl_wait();               // h (written by gate_up_gemv) is complete and visible from here on
+  for (int it = 0; it < iters; ++it) {
+    const int c0 = it * stride + (blockIdx.x * GPB + grp) * R;
+    if (c0 < d) {
+      float o[1][R];
+      const char *const base[1] = {static_cast<const char *>(wd) + c0 * pitch + static_cast<size_t>(v_lo) * 16};
+      rows_dot<true, 1, R, true, U>(base, pitch, d - c0, h + 8 * v_lo, (v_hi - v_lo) * 8, lane, o);
+      if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) part[wid][r] = o[0][r];
+      }
+    }
+    __syncthreads();
+    if (q == 0 && lane == 0 && c0 < d) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (c0 + r < d) {
+          float t = 0.f;
+#pragma unroll
+          for (int k = 0; k < KS; ++k) t += part[grp * KS + k][r];
+          const float rv = residual ? __bfloat162float(static_cast<const __nv_bfloat16 *>(residual)[c0 + r]) : 0.f;
+          static_cast<__nv_bfloat16 *>(out)[c0 + r] = __float2bfloat16_rn(rv + t);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Order-preserving map float -> uint32 (larger float -> larger key), then pack with the
 // complemented index so that the u64 max picks the largest value and, among equal
 // values, the LOWEST index.
@@ -450,6 +498,30 @@ cudaError_t launch_last_token_mlp(const void *x, const void *residual, const voi
   // for the pair (profiles/r1_gemv_variants.txt).  MOM_GEMV_VARIANT=0 restores the old shape.
   if (!is_bf16) return last_token_pair<false, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream, norm_eps);
   const int variant = gemv::env_or("MOM_GEMV_VARIANT", 2);
+  if (is_bf16 && (variant == 5 || variant == 6) && I / 8 >= 4) {
+    // gate/up as variant 2; down K-split over KS = 2 (5) or 4 (6) warps per row group
+    using namespace gemv;
+    const size_t smem1 = static_cast<size_t>(d) * sizeof(float);
+    cudaError_t e;
+    if ((e = set_smem(gate_up_gemv<true, 2, 2, 4>, smem1)) != cudaSuccess) return e;
+    const int resident = num_sms * 4 * WARPS;
+    const int groups = (I + 1) / 2, r = (groups + resident - 1) / resident;
+    const int blocks1 = ((groups + r - 1) / r + WARPS - 1) / WARPS;
+    const bool pdl = env_or("MOM_GEMV_PDL", 1) != 0;
+    if ((e = launch_maybe_pdl(gate_up_gemv<true, 2, 2, 4>, blocks1, smem1, stream, pdl, x, wg, wu, h_ws, d, I,
+                              norm_eps)) != cudaSuccess)
+      return e;
+    // single balanced wave: rows per iteration = blocks * (WARPS / KS) * 2 >= d when it fits
+    const int ks = variant == 5 ? 2 : 4;
+    const int rows_per_block = (WARPS / ks) * 2;
+    int blocks2 = (d + rows_per_block - 1) / rows_per_block;
+    if (blocks2 > num_sms * 4) blocks2 = num_sms * 4;
+    if (variant == 5)
+      return launch_maybe_pdl(down_gemv_ks<2, 4, 2, 4>, blocks2, 0, stream, pdl, static_cast<const float *>(h_ws), wd,
+                              residual, out, d, I);
+    return launch_maybe_pdl(down_gemv_ks<2, 4, 4, 4>, blocks2, 0, stream, pdl, static_cast<const float *>(h_ws), wd,
+                            residual, out, d, I);
+  }
   if (variant == 0)
     return last_token_pair<true, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream, norm_eps);
   // deeper per-lane load queues (same per-row summation order: bit-neutral): down 8 loads in flight

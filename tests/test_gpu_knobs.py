@@ -57,6 +57,38 @@ GEMV_KNOBS = [{}, {"MOM_GEMV_VARIANT": "0"}, {"MOM_GEMV_PDL": "0"}, {"MOM_GEMV_P
 GEMV_ALL = sorted({k for v in GEMV_KNOBS for k in v})
 
 
+@pytest.mark.parametrize("variant", ["5", "6"])
+@pytest.mark.parametrize("d,I", [(4096, 14336), (3584, 18944), (520, 1160), (256, 688)])
+def test_gemv_ksplit_down_variants(cuda_device, variant, d, I):
+    """MOM_GEMV_VARIANT=5 / 6: the down GEMV K-split over 2 / 4 warps per row group (a different, fixed
+    summation order): bit-identical with and without PDL, and within the bf16 bar of the oracle."""
+    import oracle
+    from tests.parity import TOL_BF16, check_close
+    bf = torch.bfloat16
+    wg, wu, wd = synth.mlp_weights(d, I, 0, cuda_device, bf)
+    x = synth.hidden(1, d, cuda_device, bf)[0]
+    res = synth.hidden(1, d, cuda_device, bf, seed=synth.SEED_X + 1)[0]
+    outs = []
+    old = {k: os.environ.get(k) for k in ("MOM_GEMV_VARIANT", "MOM_GEMV_PDL")}
+    try:
+        for knob in ({"MOM_GEMV_VARIANT": variant}, {"MOM_GEMV_VARIANT": variant, "MOM_GEMV_PDL": "0"}):
+            os.environ.pop("MOM_GEMV_PDL", None)
+            os.environ.update(knob)
+            y = torch.empty_like(x)
+            _mom.mlp_last_token(x, res, wg, wu, wd, y)
+            torch.cuda.synchronize()
+            outs.append(y)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert torch.equal(outs[0], outs[1])
+    ref = oracle.mlp_rows(x.cpu()[None], res.cpu()[None], wg.cpu(), wu.cpu(), wd.cpu(), [0])[0]
+    check_close(outs[0].cpu(), ref, TOL_BF16, f"last-token K-split{variant} d={d} I={I}")
+
+
 @pytest.mark.parametrize("d,I", [(4096, 14336), (520, 1160)])
 def test_gemv_knobs_are_bit_neutral(cuda_device, d, I):
     """Last-token GEMV shapes (rows per warp step, loads in flight, PDL, L2 prefetch) keep each
