@@ -29,8 +29,9 @@
  *               (arguments are checked before any launch).  MOM_ERR_CUDA / _NCCL report a failed
  *               launch or library call; launches of the same call that preceded it (earlier
  *               mini-sequences) stay enqueued.  mom_last_error() returns a thread-local message.
- *   Tuning      Environment knobs read per call (defaults are the measured best on B200).  None
- *               changes results -- outputs are bitwise identical for every setting (knob tests):
+ *   Tuning      Environment knobs read per call (defaults are the measured best on B200).  Apart
+ *               from MOM_GEMV_VARIANT's families (below) none changes results -- outputs are bitwise
+ *               identical for every setting (knob tests):
  *               MOM_CTA_GROUP (2)        CTAs per tcgen05 tile (cta_group::2 pair, or 1)
  *               MOM_GROUP_M_A (16), MOM_GROUP_M_B (8)   raster: row blocks per group
  *               MOM_RASTER_B_COLS (0)    phase B by groups of G output-column blocks instead
@@ -47,8 +48,11 @@
  *               MOM_NB_B (per shape)     phase-B tile width (wave quantisation)
  *               MOM_GATHER_FORWARD (1)   f1: rows of mini-sequence i-1 forwarded during i
  *               MOM_GEMV_PDL (1)         both last-token GEMVs and the argmax reduction PDL-launched
- *               MOM_GEMV_VARIANT (2)     down GEMV loads in flight per row: 2 -> 8 at 2 blocks/SM,
- *                                        1 -> 4, 0 -> 2 at 4 blocks/SM; 3 -> also gate/up at 4
+ *               MOM_GEMV_VARIANT (5)     down GEMV: 5 -> each row group K-split over 2 warps (fixed-
+ *                                        order combine), 6 -> over 4; loads in flight per row without
+ *                                        K-split: 2 -> 8 at 2 blocks/SM, 1 -> 4, 0 -> 2 at 4 blocks/SM;
+ *                                        3 -> also gate/up at 4.  5 / 6 sum in their own fixed order
+ *                                        (bit-stable per variant; 0-3 are bitwise equal to each other)
  *               MOM_GEMV_PREFETCH (0)    KB of each warp's first W_down rows prefetched to L2
  *               Numerics knob: MOM_FAST_SILU (1: the phase-A SiLU quotient by rcp.approx, <= 2 fp32
  *               ulp; 0: IEEE division, whose per-element slow-path branch serialises the epilogue).

@@ -497,7 +497,7 @@ cudaError_t launch_last_token_mlp(const void *x, const void *residual, const voi
   // 2 x 2 at 4/SM (4 MB in flight: latency-bound at ~3.5 TB/s); measured 74.8 -> 64.5-67.6 us
   // for the pair (profiles/r1_gemv_variants.txt).  MOM_GEMV_VARIANT=0 restores the old shape.
   if (!is_bf16) return last_token_pair<false, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream, norm_eps);
-  const int variant = gemv::env_or("MOM_GEMV_VARIANT", 2);
+  const int variant = gemv::env_or("MOM_GEMV_VARIANT", 5);
   if (is_bf16 && (variant == 5 || variant == 6) && I / 8 >= 4) {
     // gate/up as variant 2; down K-split over KS = 2 (5) or 4 (6) warps per row group
     using namespace gemv;
