@@ -51,9 +51,11 @@ def test_knobs_are_bit_neutral(cuda_device):
         assert torch.equal(o, outs[0]), knob
 
 
-GEMV_KNOBS = [{}, {"MOM_GEMV_VARIANT": "0"}, {"MOM_GEMV_PDL": "0"}, {"MOM_GEMV_PREFETCH": "2"},
-              {"MOM_GEMV_VARIANT": "0", "MOM_GEMV_PDL": "0"}, {"MOM_GEMV_VARIANT": "1"},
-              {"MOM_GEMV_VARIANT": "2"}, {"MOM_GEMV_VARIANT": "3"}]
+# the non-K-split family (variants 0-3) shares one summation order; the default (5) is tested in
+# test_gemv_ksplit_down_variants
+GEMV_KNOBS = [{"MOM_GEMV_VARIANT": "2"}, {"MOM_GEMV_VARIANT": "0"}, {"MOM_GEMV_VARIANT": "2", "MOM_GEMV_PDL": "0"},
+              {"MOM_GEMV_VARIANT": "2", "MOM_GEMV_PREFETCH": "2"}, {"MOM_GEMV_VARIANT": "0", "MOM_GEMV_PDL": "0"},
+              {"MOM_GEMV_VARIANT": "1"}, {"MOM_GEMV_VARIANT": "3"}]
 GEMV_ALL = sorted({k for v in GEMV_KNOBS for k in v})
 
 
