@@ -492,10 +492,11 @@ static cudaError_t last_token_pair(const void *x, const void *residual, const vo
 cudaError_t launch_last_token_mlp(const void *x, const void *residual, const void *wg, const void *wu,
                                   const void *wd, void *out, float *h_ws, int d, int I, bool is_bf16, int num_sms,
                                   cudaStream_t stream, float norm_eps) {
-  // (rows per warp step, 16-B loads in flight per row, min blocks per SM) for gate/up and down.
-  // Down: 2 rows x 4 loads in flight at 2 blocks/SM (2048 warps, 16 MB in flight) instead of
-  // 2 x 2 at 4/SM (4 MB in flight: latency-bound at ~3.5 TB/s); measured 74.8 -> 64.5-67.6 us
-  // for the pair (profiles/r1_gemv_variants.txt).  MOM_GEMV_VARIANT=0 restores the old shape.
+  // Default (MOM_GEMV_VARIANT=5, bf16): gate/up 2 rows x 2 x 2 loads in flight at 4 blocks/SM, down
+  // K-split over 2 warps per 2-row group (profiles/r2_gemv_ksplit_ab.txt).  Variants 0-3: the
+  // un-split down GEMV with (rows per warp step, 16-B loads in flight per row, min blocks per SM) =
+  // (2, 2, 4) / (2, 4, 2) / (2, 8, 2) -- 2 x 2 at 4/SM had 4 MB in flight and was latency-bound at
+  // ~3.5 TB/s (profiles/r1_gemv_variants.txt).  fp32: the pair with (2, 2, 4).
   if (!is_bf16) return last_token_pair<false, 2, 2, 4, 2, 2, 4>(x, residual, wg, wu, wd, out, h_ws, d, I, num_sms, stream, norm_eps);
   const int variant = gemv::env_or("MOM_GEMV_VARIANT", 5);
   if (is_bf16 && (variant == 5 || variant == 6) && I / 8 >= 4) {
