@@ -557,15 +557,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t idesc_b = ptx::idesc_bf16_f32(BM * CG, p.nb);
       uint32_t stage = 0, phase = 0;
       uint32_t acc = 0, acc_phase = 0;
+#ifdef MOM_TRACE_WAITS
+      // probe build (-DMOM_TRACE_WAITS): MMA-issuer cycles spent waiting for operands (full) and for a
+      // free accumulator (tempty), after the first stage of the launch; written to trace slots 6 / 7
+      unsigned long long wait_full = 0, wait_acc = 0;
+#endif
       for (uint32_t t = cluster_id; t < num_tiles; t += num_clusters) {
         const Tile tl = decode_tile<MODE>(t, p);
         const uint32_t num_kb = tl.a ? kbA : kbB;
         const uint32_t idesc = tl.a ? (tl.hw < BHALF ? idesc_a_half : idesc_a) : idesc_b;
+#ifdef MOM_TRACE_WAITS
+        const long long w0 = clock64();
+#endif
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+#ifdef MOM_TRACE_WAITS
+        if (p.trace && t != cluster_id) wait_acc += clock64() - w0;
+#endif
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * ACC_COLS;
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
+#ifdef MOM_TRACE_WAITS
+          const long long w1 = clock64();
+#endif
           ptx::mbar_wait(&full[stage], phase);
+#ifdef MOM_TRACE_WAITS
+          if (p.trace && (t != cluster_id || kb != 0)) wait_full += clock64() - w1;
+#endif
           ptx::tc_fence_after();
           if (p.trace && kb == 0 && t == cluster_id) {  // first MMA: time and SM cycle counter
             p.trace[blockIdx.x * 8 + 1] = globaltimer_ns();
@@ -587,6 +604,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (p.trace) {  // last MMA issued
         p.trace[blockIdx.x * 8 + 2] = globaltimer_ns();
         p.trace[blockIdx.x * 8 + 5] = clock64();
+#ifdef MOM_TRACE_WAITS
+        p.trace[blockIdx.x * 8 + 6] = wait_full;
+        p.trace[blockIdx.x * 8 + 7] = wait_acc;
+#endif
       }
     }
   } else if (warp >= EPI_WARP0) {
@@ -616,10 +637,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         epilogue_a<false>(p, taddr, row, row_ok, tl.c0, tl.hw);
       else
         epilogue_b(p, taddr, row - lane, tl.n * p.nb, epi_stage + q * 32 * 128);
+#ifndef MOM_TRACE_WAITS
       if (p.trace && q == 0 && lane == 0) {  // epilogue cycles of warp 4 (summed) and tile count
         p.trace[blockIdx.x * 8 + 6] += clock64() - epi_t0;
         p.trace[blockIdx.x * 8 + 7] += 1;
       }
+#endif
       // release the accumulator to the MMA issuer
       ptx::tc_fence_before();
       __syncwarp();
