@@ -59,7 +59,9 @@ def load_peaks():
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 200 for the single-layer bench, so the timed region is >= 3 s of "
+                         "back-to-back steps -- the sustained power state a serving GPU runs in; 20 for --stack)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["mine", "reference"], default="mine")
     ap.add_argument("--config", type=int, default=1, help="index into BASELINE.json configs (default 1 = config 2)")
@@ -857,6 +859,10 @@ def run_mine(args):
         result["e2e"] = {"value": total_tokens / (e_ms / 1e3), "unit": "tokens/s",
                          "h2d_bytes_per_step": int(world * wl.x.numel() * 2),
                          "d2h_bytes_per_step": int(wl.V * 4 + 4), "ms_per_step": e_ms,
+                         # the host link also carries the method's own copies every step: Alg. 1's KV
+                         # reload (H2D) beside x, the offload (D2H); at steady state the H2D direction
+                         # (x + KV) is the e2e bound
+                         "pcie_h2d_gbs_incl_kv_reload": (wl.x.numel() + wl.kv.numel()) * 2 / (e_ms * 1e-3) / 1e9,
                          "result_read_back": "the last token's logits + greedy token (Alg. 1 returns L, P:107); "
                                              "the [S, d] MLP output stays in HBM as the next layer's input"}
 
@@ -1175,6 +1181,8 @@ def run_reference(args):
 
 def main():
     args = parse_args()
+    if args.steps is None:
+        args.steps = 20 if args.stack else 200
     if args.impl == "reference":
         run_reference(args)
     elif args.stack:
