@@ -1179,10 +1179,16 @@ def run_reference(args):
     print(json.dumps(res), flush=True)
 
 
-def main():
-    args = parse_args()
+def resolve_defaults(args):
+    """--steps defaults per mode: 200 single-layer steps (a >= 3 s timed region at config 2, so the
+    roofline compares with the sustained cuBLAS figure), 20 for the --stack runs (seconds per step)."""
     if args.steps is None:
         args.steps = 20 if args.stack else 200
+    return args
+
+
+def main():
+    args = resolve_defaults(parse_args())
     if args.impl == "reference":
         run_reference(args)
     elif args.stack:

@@ -54,3 +54,15 @@ def test_trace_efficiency_on_synthetic_stamps():
     fpc_a = 4.0 * S * d * I / (sms * (idealA + 1_000))
     assert r["phaseA_flop_per_sm_cycle"] == pytest.approx(fpc_a, rel=1e-3)
     assert r["mlp_step_mma_issue_efficiency"] == pytest.approx((idealA + idealB) / (idealA + 5_000 + idealB), abs=1e-4)
+
+
+def test_default_steps_make_a_sustained_region(monkeypatch):
+    """No flags: 200 timed config-2 steps (~17 ms each -> >= 3 s, the region length from which bench.py
+    divides by the sustained peak); --stack: 20; an explicit --steps wins."""
+    monkeypatch.setattr(sys, "argv", ["bench.py"])
+    assert bench.resolve_defaults(bench.parse_args()).steps == 200
+    assert 200 * 16.4e-3 >= 3.0
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--stack"])
+    assert bench.resolve_defaults(bench.parse_args()).steps == 20
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--steps", "7"])
+    assert bench.resolve_defaults(bench.parse_args()).steps == 7
