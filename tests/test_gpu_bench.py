@@ -34,6 +34,9 @@ def test_bench_single_gpu_contract(cuda_device):
     assert res["roofline"]["bound"] == "tensor" and 0 < res["roofline"]["frac"] < 1.5
     assert res["gpu_launches"] == 3 * (2 * res["config"]["M"] + 4)
     assert res["e2e"]["h2d_bytes_per_step"] > 0 and res["e2e"]["value"] > 0
+    assert 0 < res["e2e"]["pcie_h2d_gbs_incl_kv_reload"] < 200  # host-link rate: physical (PCIe Gen5 x16)
+    # a 3-step region is far below 3 s: the roofline compares with the burst figure
+    assert "burst" in res["roofline"]["peak_source"] and res["roofline"]["frac"] == res["roofline"]["frac_of_burst_peak"]
     assert res["serial"]["value"] > 0
     assert res["activation_reduction_x"] > res["config"]["M"] * 0.99
     kt = res["kernel_trace"]  # in-kernel timeline: clocks and MMA-issue efficiency are physical
