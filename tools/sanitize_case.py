@@ -1,6 +1,6 @@
 """Small tcgen05 MLP calls for compute-sanitizer: ragged mini-sequences with phase-A half-width tail
 tiles (S=2000, C=600, I=4096), both CTA-group modes, the fused single-launch mode, the f1 gather into
-two local peer buffers, plus the last-token GEMVs and the LM head."""
+two local peer buffers, plus the last-token GEMVs, the LM head and the fp32 SIMT path."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -45,4 +45,11 @@ logits = torch.empty(1000, dtype=torch.float32, device=dev)
 am = torch.empty(1, dtype=torch.int32, device=dev)
 _mom.lm_head_last(y, synth.norm_gain(d, dev, bf), 1e-5, wh, logits, am)
 torch.cuda.synchronize()
-print("sanitize case OK", float(out.float().abs().mean()), int(am.item()))
+# fp32 SIMT path (double-buffered K tiles, ragged K tail: I = 688 is not a multiple of the 32-wide K tile)
+d32, I32 = 256, 688
+wg32, wu32, wd32 = synth.mlp_weights(d32, I32, 0, dev, torch.float32)
+x32 = synth.hidden(300, d32, dev, torch.float32)
+out32 = torch.empty_like(x32)
+_mom.mlp_minseq_fwd(x32, x32, wg32, wu32, wd32, out32, 128)
+torch.cuda.synchronize()
+print("sanitize case OK", float(out.float().abs().mean()), int(am.item()), float(out32.abs().mean()))
